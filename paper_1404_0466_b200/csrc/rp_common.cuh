@@ -1,0 +1,72 @@
+// Shared device helpers for the piCholesky CV path on B200 (sm_100a).
+//
+// FP64 on sm_100a: tcgen05 has no f64 kind, so the FP64 tensor path is the
+// warp-level mma.sync m8n8k4 f64 (SASS DMMA.8x8x4). Measured on this pool's
+// B200 (tools/fp64_peaks.cu, profiles/r01_fp64_peaks.json): DMMA 37.0 TFLOP/s,
+// DFMA 33.6 TFLOP/s, and the two share one FP64 datapath (mixed 31.6 + 4.0).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RP_DEVINL __device__ __forceinline__
+
+namespace rp {
+
+// D = A(8x4, row) * B(4x8, col) + D.  Fragment ownership per lane
+// (g = lane >> 2, t = lane & 3):  a = A[g][t], b = B[t][g], d0/d1 = D[g][2t], D[g][2t+1].
+RP_DEVINL void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+RP_DEVINL uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 8-byte async copy global -> shared, zero-filled when !valid.
+RP_DEVINL void cp_async8(void* smem, const void* gmem, bool valid) {
+  int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n));
+}
+
+// 16-byte async copy (L2 only), zero-filled when !valid.
+RP_DEVINL void cp_async16(void* smem, const void* gmem, bool valid) {
+  int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(n));
+}
+
+RP_DEVINL void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+RP_DEVINL void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace rp
+
+// Status codes of the C ABI (include/ridgepath_b200.h).
+#define RP_OK 0
+#define RP_EINVAL (-1)
+#define RP_ECUDA 1
+
+// ---- host-side error plumbing shared by the C-ABI translation units ----
+namespace rp {
+int set_error(int code, const char* fmt, ...);  // records rp_last_error(), returns code
+inline int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return RP_OK;
+  return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
+}
+}  // namespace rp
+
+#define RP_LAUNCH_CHECK(where)                          \
+  do {                                                  \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return rp::cuda_status(_e, where); \
+  } while (0)
+
+#define RP_REQUIRE(cond, ...)                                  \
+  do {                                                         \
+    if (!(cond)) return rp::set_error(RP_EINVAL, __VA_ARGS__); \
+  } while (0)

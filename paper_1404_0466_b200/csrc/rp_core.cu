@@ -1,0 +1,692 @@
+// C-ABI entry points for the piCholesky CV path (everything except the fused eval+solve,
+// which lives in rp_solve.cu). See include/ridgepath_b200.h for the contract and the
+// reference routine each entry point replaces.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "rp_common.cuh"
+#include "rp_gemm.cuh"
+#include "../../include/ridgepath_b200.h"
+
+namespace rp {
+
+static thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// ------------------------------------------------------------------ GEMM dispatch
+
+template <int AL, int BM, int BN, int WM, int WN, int EPI>
+static int gemm(const GemmArgs& a, int batch, cudaStream_t st, const char* name) {
+  if (a.M <= 0 || a.N <= 0 || batch <= 0) return RP_OK;
+  bool vec2 = aligned16(a.A) && aligned16(a.B) && a.lda % 2 == 0 && a.ldb % 2 == 0 && a.strideA % 2 == 0 &&
+              a.strideB % 2 == 0 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0);
+  const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
+  if (a.lower_only && (BM != BN || a.M != a.N)) return set_error(RP_EINVAL, "%s: lower_only needs square", name);
+  dim3 grid(a.lower_only ? mt * (mt + 1) / 2 : mt * nt, batch);
+  size_t smem = GemmSmem<AL, BM, BN>::BYTES;
+  if (vec2) {
+    auto k = dgemm_kernel<AL, BM, BN, WM, WN, EPI, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(a);
+  } else {
+    auto k = dgemm_kernel<AL, BM, BN, WM, WN, EPI, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, 256, smem, st>>>(a);
+  }
+  RP_LAUNCH_CHECK(name);
+  return RP_OK;
+}
+
+static GemmArgs gemm_args() {
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.alpha = 1.0;
+  a.beta = 0.0;
+  return a;
+}
+
+// ------------------------------------------------------------------ small kernels
+
+// Lower-triangle mirror, 32x32 tiles through shared memory.
+__global__ void symmetrize_kernel(double* G, int d, int64_t stride) {
+  __shared__ double tile[32][33];
+  const int nt = (d + 31) / 32;
+  int lin = blockIdx.x;
+  int I = (int)((sqrt(8.0 * lin + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= lin) ++I;
+  while (I * (I + 1) / 2 > lin) --I;
+  int J = lin - I * (I + 1) / 2;
+  if (I >= nt) return;
+  double* A = G + blockIdx.y * stride;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    int row = I * 32 + tx, col = J * 32 + r;  // element (row, col) of the lower block (I, J)
+    tile[r][tx] = (row < d && col < d) ? A[(int64_t)col * d + row] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    // write (J*32 + tx, I*32 + r) = (I*32 + r, J*32 + tx)
+    int row = J * 32 + tx, col = I * 32 + r;
+    if (row < d && col < d && row < col) A[(int64_t)col * d + row] = tile[tx][r];
+  }
+}
+
+struct FoldSysArgs {
+  int folds[64];
+  double lams[32];
+};
+
+__global__ void gram_sum_kernel(const double* G, int nblocks, int d, double* Gsum) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t n = (int64_t)d * d;
+  if (e >= n) return;
+  int i = (int)(e % d), j = (int)(e / d);
+  if (i < j) return;
+  double s = 0.0;
+  for (int b = 0; b < nblocks; ++b) s += G[b * n + e];
+  Gsum[e] = s;
+}
+
+__global__ void fold_shift_kernel(const double* Gsum, const double* G, int d, int s, FoldSysArgs fa, double* A) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t n = (int64_t)d * d;
+  if (e >= n) return;
+  int i = (int)(e % d), j = (int)(e / d);
+  if (i < j) return;
+  const int fs = blockIdx.y, f = fs / s, si = fs % s;
+  double v = Gsum[e] - G[fa.folds[f] * n + e];
+  if (i == j) v += fa.lams[si];
+  A[fs * n + e] = v;
+}
+
+__global__ void fold_rhs_kernel(const double* C, int nblocks, int d, int dp, int m, FoldSysArgs fa, double* rhs) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;  // over dp*m, row-major (i, o)
+  if (e >= dp * m) return;
+  const int f = blockIdx.y;
+  int i = e / m, o = e % m;
+  double v = 0.0;
+  if (i < d) {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s += C[((int64_t)b * m + o) * d + i];
+    v = s - C[((int64_t)fa.folds[f] * m + o) * d + i];
+  }
+  rhs[(int64_t)f * dp * m + e] = v;
+}
+
+// Column sums of squares per fold block: yy[b][o] = sum_rows Y[row][o]^2 (fixed row order per thread
+// chunk, then a fixed-order combine).
+__global__ void col_sumsq_kernel(const double* Y, int64_t ldy, int64_t rows, int m, double* yy) {
+  const int b = blockIdx.x, o = blockIdx.y;
+  const double* y = Y + (int64_t)b * rows * ldy + o;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t r = threadIdx.x; r < rows; r += 256) {
+    double v = y[r * ldy];
+    s = fma(v, v, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) yy[b * m + o] = red[0];
+}
+
+// ------------------------------------------------------------------ Cholesky
+
+constexpr int CHOL_NB = 128;
+
+// Factor the NB x NB diagonal block at (k0, k0) of every batch matrix in shared memory
+// (unblocked right-looking, LAPACK dpotf2 order: sqrt pivot, scale by reciprocal, rank-1 update),
+// write L11 back, and write inv(L11) (column-major NB x NB, zero above the diagonal) to `inv`
+// for the panel TRSM, which then runs as a DMMA GEMM.
+__global__ void __launch_bounds__(1024) potrf_diag_kernel(double* A, int d, int64_t stride, int k0, double* inv,
+                                                          int* info) {
+  constexpr int NB = CHOL_NB;
+  extern __shared__ double a[];  // NB*NB column-major
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (info[b] != 0) return;
+  double* Ab = A + b * stride;
+  const int nbv = min(NB, d - k0);
+  for (int e = tid; e < NB * NB; e += 1024) {
+    int i = e % NB, j = e / NB;
+    double v;
+    if (i < nbv && j < nbv) v = (i >= j) ? Ab[(int64_t)(k0 + j) * d + k0 + i] : 0.0;
+    else v = (i == j) ? 1.0 : 0.0;
+    a[e] = v;
+  }
+  __syncthreads();
+  for (int j = 0; j < nbv; ++j) {
+    const double ajj = a[j * NB + j];
+    if (!(ajj > 0.0)) {
+      if (tid == 0) info[b] = k0 + j + 1;
+      return;
+    }
+    const double ljj = sqrt(ajj);
+    const double rl = 1.0 / ljj;
+    for (int i = j + 1 + tid; i < nbv; i += 1024) a[j * NB + i] *= rl;
+    __syncthreads();
+    if (tid == 0) a[j * NB + j] = ljj;
+    const int n1 = nbv - j - 1;
+    for (int e = tid; e < n1 * n1; e += 1024) {
+      const int c = e / n1, i = e - c * n1;
+      if (i >= c) a[(j + 1 + c) * NB + j + 1 + i] -= a[j * NB + j + 1 + i] * a[j * NB + j + 1 + c];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < NB * NB; e += 1024) {
+    int i = e % NB, j = e / NB;
+    if (i < nbv && j < nbv && i >= j) Ab[(int64_t)(k0 + j) * d + k0 + i] = a[e];
+  }
+  // inv(L11): warp w solves columns c = w, w+32, ...; lane owns rows lane + 32 r.
+  double* X = inv + (int64_t)b * NB * NB;
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int c = warp; c < nbv; c += 32) {
+    double acc[NB / 32];
+#pragma unroll
+    for (int r = 0; r < NB / 32; ++r) acc[r] = 0.0;
+    for (int k = lane; k < c; k += 32) X[(int64_t)c * NB + k] = 0.0;
+    for (int k = c; k < nbv; ++k) {
+      const int owner = k & 31, rk = k >> 5;
+      double mine = 0.0;
+#pragma unroll
+      for (int r = 0; r < NB / 32; ++r)
+        if (r == rk) mine = acc[r];
+      double xk = ((k == c ? 1.0 : 0.0) - mine) / a[k * NB + k];
+      xk = __shfl_sync(0xffffffffu, xk, owner);
+      if (lane == owner) X[(int64_t)c * NB + k] = xk;
+#pragma unroll
+      for (int r = 0; r < NB / 32; ++r) {
+        const int i = lane + 32 * r;
+        if (i > k && i < nbv) acc[r] = fma(a[k * NB + i], xk, acc[r]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ fit
+
+struct FitArgs {
+  double P[5][32];  // (r+1) x s
+  double V[32][5];  // s x (r+1)
+};
+
+__global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles, FitArgs fa, double* theta,
+                                 double* partial) {
+  const int64_t tile = blockIdx.x;
+  const int f = blockIdx.y;
+  const int P = r + 1;
+  int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
+  while ((int64_t)I * (I + 1) / 2 > tile) --I;
+  const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  const int64_t n = (int64_t)d * d;
+  const double* Lf = L + (int64_t)f * s * n;
+  double* out = theta + ((int64_t)f * ntiles + tile) * P * 4096;
+  double res = 0.0;
+  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+    const int j = e >> 6, i = e & 63;
+    const int row = I * 64 + i, col = J * 64 + j;
+    if (row < d && col < d && row >= col) {
+      double T[32];
+      for (int si = 0; si < s; ++si) T[si] = Lf[si * n + (int64_t)col * d + row];
+      double th[5];
+      for (int p = 0; p < P; ++p) {
+        double v = 0.0;
+        for (int si = 0; si < s; ++si) v = fma(fa.P[p][si], T[si], v);
+        th[p] = v;
+        out[p * 4096 + e] = v;
+      }
+      for (int si = 0; si < s; ++si) {
+        double v = 0.0;
+        for (int p = 0; p < P; ++p) v = fma(fa.V[si][p], th[p], v);
+        double dlt = T[si] - v;
+        res = fma(dlt, dlt, res);
+      }
+    } else {
+      const double diag = (row == col && row >= d) ? 1.0 : 0.0;
+      for (int p = 0; p < P; ++p) out[p * 4096 + e] = (p == 0) ? diag : 0.0;
+    }
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = res;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(int64_t)f * ntiles + tile] = red[0];
+}
+
+__global__ void fit_resid_kernel(const double* partial, int64_t ntiles, double* resid) {
+  const int f = blockIdx.x;
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < ntiles; i += 256) s += partial[f * ntiles + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) resid[f] = sqrt(red[0]);
+}
+
+RP_DEVINL int64_t tile_offset(int row, int col, int P) {
+  const int I = row >> 6, J = col >> 6;
+  return ((int64_t)I * (I + 1) / 2 + J) * P * 4096 + (col & 63) * 64 + (row & 63);
+}
+
+// pichol.eval_vector's arithmetic exactly (pichol.py:147-150): v = theta_r; v *= t; v += theta_i,
+// with separate roundings (no FMA contraction).
+RP_DEVINL double horner_ref(const double* th, int P, double t) {
+  double v = th[(int64_t)(P - 1) * 4096];
+  for (int p = P - 2; p >= 0; --p) v = __dadd_rn(__dmul_rn(v, t), th[(int64_t)p * 4096]);
+  return v;
+}
+
+__global__ void materialize_kernel(const double* theta, int d, int P, double t, double* L) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)d * d) return;
+  int row = (int)(e % d), col = (int)(e / d);
+  L[e] = (row >= col) ? horner_ref(theta + tile_offset(row, col, P), P, t) : 0.0;
+}
+
+__global__ void export_kernel(const double* theta, int d, int P, const int64_t* perm, int64_t D, double* out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= D) return;
+  int64_t pos = perm ? perm[j] : j;
+  int row = (int)(pos % d), col = (int)(pos / d);
+  for (int p = 0; p < P; ++p) out[p * D + j] = (row >= col) ? theta[tile_offset(row, col, P) + (int64_t)p * 4096] : 0.0;
+}
+
+__global__ void theta_init_kernel(double* theta, int d, int P, int64_t ntiles) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= ntiles * P * 4096) return;
+  int64_t tile = e / (P * 4096);
+  int rem = (int)(e % (P * 4096));
+  int p = rem / 4096, w = rem % 4096;
+  int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
+  while ((int64_t)I * (I + 1) / 2 > tile) --I;
+  int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  int row = I * 64 + (w & 63), col = J * 64 + (w >> 6);
+  theta[e] = (p == 0 && row == col && row >= d) ? 1.0 : 0.0;
+}
+
+__global__ void import_kernel(const double* vec, int d, int P, const int64_t* perm, int64_t D, double* theta) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= D) return;
+  int64_t pos = perm ? perm[j] : j;
+  int row = (int)(pos % d), col = (int)(pos / d);
+  if (row < col) return;
+  for (int p = 0; p < P; ++p) theta[tile_offset(row, col, P) + (int64_t)p * 4096] = vec[p * D + j];
+}
+
+// ------------------------------------------------------------------ hold-out reductions
+
+// sse[f][n] = sum_tm partial[f][tm][n] (fixed order), then curves[f][j][o] from it.
+__global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, int m, int64_t n_val, int metric,
+                                      const double* yy, const double* bc, double* curves) {
+  const int f = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int tm = 0; tm < mtiles; ++tm) s += partial[((int64_t)f * mtiles + tm) * N + n];
+  double out;
+  if (yy) {  // Gram form: n_val * MSE = y^T y - 2 w^T c + w^T G w
+    const int o = n % m;
+    double sse = yy[f * m + o] - 2.0 * bc[(int64_t)f * N + n] + s;
+    out = sqrt((sse > 0.0 ? sse : 0.0) / (double)n_val);
+  } else if (metric == RP_METRIC_RMSE) {
+    out = sqrt(s / (double)n_val);
+  } else {
+    out = s / (double)n_val;
+  }
+  curves[(int64_t)f * N + n] = out;
+}
+
+// bc[f][n] = sum_i W[i][n] * C_f[i][o]
+__global__ void holdout_bc_kernel(const double* W, int64_t ldw, int64_t w_fold_stride, const double* Cf,
+                                  int64_t c_stride, int d, int m, int N, double* bc) {
+  const int f = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int o = n % m;
+  const double* w = W + f * w_fold_stride + n;
+  const double* c = Cf + f * c_stride + (int64_t)o * d;
+  double s0 = 0.0, s1 = 0.0;
+  int i = 0;
+  for (; i + 2 <= d; i += 2) {
+    s0 = fma(w[(int64_t)i * ldw], c[i], s0);
+    s1 = fma(w[(int64_t)(i + 1) * ldw], c[i + 1], s1);
+  }
+  if (i < d) s0 = fma(w[(int64_t)i * ldw], c[i], s0);
+  bc[(int64_t)f * N + n] = s0 + s1;
+}
+
+__global__ void select_kernel(const double* curves, int k, int q, int m, double* mean, int* best) {
+  const int N = q * m;
+  for (int e = threadIdx.x; e < N; e += blockDim.x) {
+    double s = 0.0;
+    for (int f = 0; f < k; ++f) s += curves[(int64_t)f * N + e];
+    mean[e] = s / (double)k;
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < m; o += blockDim.x) {
+    int bi = 0;
+    double bv = mean[o];
+    if (!isnan(bv)) {
+      for (int j = 1; j < q; ++j) {
+        double v = mean[j * m + o];
+        if (isnan(v)) {
+          bi = j;
+          break;
+        }
+        if (v < bv) {
+          bv = v;
+          bi = j;
+        }
+      }
+    }
+    best[o] = bi;
+  }
+}
+
+}  // namespace rp
+
+using namespace rp;
+
+static inline int grid1d(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
+
+extern "C" {
+
+int rp_version(void) { return 1; }
+
+const char* rp_last_error(void) { return rp::g_last_error.c_str(); }
+
+int64_t rp_tile_count(int d) {
+  int64_t nt = (d + 63) / 64;
+  return nt * (nt + 1) / 2;
+}
+
+int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d, const double* Y,
+                   int64_t ldy, int m, double* G, double* C, void* stream) {
+  RP_REQUIRE(d >= 1 && nblocks >= 1 && rows_per_block >= 1 && ldx >= d, "rp_gram_blocks: bad sizes");
+  RP_REQUIRE(rows_per_block <= 0x7fffffff, "rp_gram_blocks: block too tall");
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmArgs a = gemm_args();
+  a.M = a.N = d;
+  a.K = (int)rows_per_block;
+  a.A = a.B = X;
+  a.lda = a.ldb = ldx;
+  a.strideA = a.strideB = rows_per_block * ldx;
+  a.C = G;
+  a.ldc = d;
+  a.strideC = (int64_t)d * d;
+  a.lower_only = 1;
+  int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
+  if (rc) return rc;
+  if (m > 0 && C != nullptr) {
+    RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
+    GemmArgs b = gemm_args();
+    b.M = d;
+    b.N = m;
+    b.K = (int)rows_per_block;
+    b.A = X;
+    b.lda = ldx;
+    b.strideA = rows_per_block * ldx;
+    b.B = Y;
+    b.ldb = ldy;
+    b.strideB = rows_per_block * ldy;
+    b.C = C;
+    b.ldc = d;
+    b.strideC = (int64_t)d * m;
+    rc = gemm<A_KMAJOR, 128, 16, 16, 16, EPI_STORE>(b, nblocks, st, "gram xty");
+  }
+  return rc;
+}
+
+int rp_symmetrize(double* G, int d, int64_t stride, int nmat, void* stream) {
+  RP_REQUIRE(d >= 1 && nmat >= 1, "rp_symmetrize: bad sizes");
+  const int nt = (d + 31) / 32;
+  dim3 grid(nt * (nt + 1) / 2, nmat);
+  symmetrize_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(G, d, stride);
+  RP_LAUNCH_CHECK("symmetrize");
+  return RP_OK;
+}
+
+int rp_col_sumsq(const double* Y, int64_t ldy, int64_t rows_per_block, int nblocks, int m, double* yy,
+                 void* stream) {
+  RP_REQUIRE(m >= 1 && nblocks >= 1 && rows_per_block >= 1, "rp_col_sumsq: bad sizes");
+  col_sumsq_kernel<<<dim3(nblocks, m), 256, 0, (cudaStream_t)stream>>>(Y, ldy, rows_per_block, m, yy);
+  RP_LAUNCH_CHECK("col_sumsq");
+  return RP_OK;
+}
+
+int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m, const int* folds_host, int nf,
+                    const double* lams_host, int s, double* Gsum, double* A, double* rhs, void* stream) {
+  RP_REQUIRE(nf >= 1 && nf <= 64 && s >= 1 && s <= 32, "rp_fold_systems: nf=%d (<=64), s=%d (<=32)", nf, s);
+  FoldSysArgs fa;
+  for (int f = 0; f < nf; ++f) {
+    RP_REQUIRE(folds_host[f] >= 0 && folds_host[f] < nblocks, "rp_fold_systems: fold %d", folds_host[f]);
+    fa.folds[f] = folds_host[f];
+  }
+  for (int i = 0; i < s; ++i) fa.lams[i] = lams_host[i];
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = (int64_t)d * d;
+  gram_sum_kernel<<<grid1d(n), 256, 0, st>>>(G, nblocks, d, Gsum);
+  RP_LAUNCH_CHECK("gram_sum");
+  if (A) {
+    fold_shift_kernel<<<dim3(grid1d(n), nf * s), 256, 0, st>>>(Gsum, G, d, s, fa, A);
+    RP_LAUNCH_CHECK("fold_shift");
+  }
+  if (rhs && m > 0) {
+    const int dp = ((d + 63) / 64) * 64;
+    fold_rhs_kernel<<<dim3(grid1d((int64_t)dp * m), nf), 256, 0, st>>>(C, nblocks, d, dp, m, fa, rhs);
+    RP_LAUNCH_CHECK("fold_rhs");
+  }
+  return RP_OK;
+}
+
+size_t rp_potrf_workspace_size(int d, int batch) {
+  (void)d;
+  return sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB;
+}
+
+int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, void* work, void* stream) {
+  RP_REQUIRE(d >= 1 && batch >= 1 && stride >= (int64_t)d * d, "rp_potrf_batched: bad sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  double* inv = (double*)work;
+  cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int) * batch, st);
+  if (e != cudaSuccess) return cuda_status(e, "potrf memset");
+  const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
+  cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int k0 = 0; k0 < d; k0 += CHOL_NB) {
+    const int nbv = d - k0 < CHOL_NB ? d - k0 : CHOL_NB;
+    potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k0, inv, info);
+    RP_LAUNCH_CHECK("potrf_diag");
+    const int rem = d - k0 - nbv;
+    if (rem <= 0) break;
+    double* L21 = A + (int64_t)k0 * d + k0 + nbv;
+    // L21 = A21 * inv(L11)^T   (in place: each CTA owns whole rows since BN >= NB)
+    GemmArgs t = gemm_args();
+    t.M = rem;
+    t.N = nbv;
+    t.K = nbv;
+    t.A = L21;
+    t.lda = d;
+    t.strideA = stride;
+    t.B = inv;
+    t.ldb = CHOL_NB;
+    t.strideB = CHOL_NB * CHOL_NB;
+    t.C = L21;
+    t.ldc = d;
+    t.strideC = stride;
+    int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(t, batch, st, "potrf trsm");
+    if (rc) return rc;
+    // A22 -= L21 L21^T (lower tiles)
+    GemmArgs u = gemm_args();
+    u.M = u.N = rem;
+    u.K = nbv;
+    u.A = u.B = L21;
+    u.lda = u.ldb = d;
+    u.strideA = u.strideB = stride;
+    u.C = A + (int64_t)(k0 + nbv) * d + k0 + nbv;
+    u.ldc = d;
+    u.strideC = stride;
+    u.alpha = -1.0;
+    u.beta = 1.0;
+    u.lower_only = 1;
+    rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf syrk");
+    if (rc) return rc;
+  }
+  return RP_OK;
+}
+
+size_t rp_fit_workspace_size(int d, int nf) { return sizeof(double) * (size_t)rp_tile_count(d) * nf; }
+
+int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_host, const double* V_host,
+                 double* theta, double* resid, void* work, void* stream) {
+  RP_REQUIRE(d >= 1 && nf >= 1 && s >= 1 && s <= 32 && r >= 0 && r <= 4, "rp_fit_tiles: bad sizes");
+  FitArgs fa;
+  memset(&fa, 0, sizeof(fa));
+  for (int p = 0; p <= r; ++p)
+    for (int i = 0; i < s; ++i) {
+      fa.P[p][i] = P_host[p * s + i];
+      fa.V[i][p] = V_host[i * (r + 1) + p];
+    }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nt = rp_tile_count(d);
+  fit_tiles_kernel<<<dim3((unsigned)nt, nf), 256, 0, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
+  RP_LAUNCH_CHECK("fit_tiles");
+  if (resid) {
+    fit_resid_kernel<<<nf, 256, 0, st>>>((double*)work, nt, resid);
+    RP_LAUNCH_CHECK("fit_resid");
+  }
+  return RP_OK;
+}
+
+int rp_eval_materialize(const double* theta, int d, int r, double t, double* L, void* stream) {
+  RP_REQUIRE(d >= 1 && r >= 0 && r <= 4, "rp_eval_materialize: bad sizes");
+  materialize_kernel<<<grid1d((int64_t)d * d), 256, 0, (cudaStream_t)stream>>>(theta, d, r + 1, t, L);
+  RP_LAUNCH_CHECK("materialize");
+  return RP_OK;
+}
+
+int rp_theta_export(const double* theta, int d, int r, const int64_t* perm, int64_t D, double* out, void* stream) {
+  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0 && r <= 4, "rp_theta_export: bad sizes");
+  export_kernel<<<grid1d(D), 256, 0, (cudaStream_t)stream>>>(theta, d, r + 1, perm, D, out);
+  RP_LAUNCH_CHECK("theta_export");
+  return RP_OK;
+}
+
+int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_t D, double* theta, void* stream) {
+  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0 && r <= 4, "rp_theta_import: bad sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = rp_tile_count(d) * (r + 1) * 4096;
+  theta_init_kernel<<<grid1d(n), 256, 0, st>>>(theta, d, r + 1, rp_tile_count(d));
+  RP_LAUNCH_CHECK("theta_init");
+  import_kernel<<<grid1d(D), 256, 0, st>>>(vec, d, r + 1, perm, D, theta);
+  RP_LAUNCH_CHECK("theta_import");
+  return RP_OK;
+}
+
+size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf) {
+  const int64_t N = (int64_t)q * m;
+  const int64_t mt_direct = (n_val + 127) / 128, mt_gram = (d + 127) / 128;
+  const int64_t mt = mt_direct > mt_gram ? mt_direct : mt_gram;
+  return sizeof(double) * (size_t)(nf * mt * N + nf * N);
+}
+
+int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows, int64_t n_val, int d,
+                      const double* Yval, int64_t ldy, int m, const double* W, int64_t ldw, int64_t w_fold_stride,
+                      int q, int nf, int metric, double* curves, void* work, void* stream) {
+  RP_REQUIRE(n_val >= 1, "rp_holdout_direct: empty validation set");
+  RP_REQUIRE(metric == RP_METRIC_RMSE || metric == RP_METRIC_MISCLASS, "rp_holdout_direct: metric %d", metric);
+  RP_REQUIRE(n_val <= 0x7fffffff && (int64_t)q * m <= 0x7fffffff, "rp_holdout_direct: sizes");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = q * m;
+  double* partial = (double*)work;
+  GemmArgs a = gemm_args();
+  a.M = (int)n_val;
+  a.N = N;
+  a.K = d;
+  a.A = Xval;
+  a.lda = ldx;
+  a.strideA = fold_stride_rows * ldx;
+  a.B = W;
+  a.ldb = ldw;
+  a.strideB = w_fold_stride;
+  a.Y = Yval;
+  a.ldy = ldy;
+  a.strideY = fold_stride_rows * ldy;
+  a.ycols = m;
+  a.partial = partial;
+  int rc = metric == RP_METRIC_RMSE ? gemm<A_MMAJOR, 128, 128, 64, 32, EPI_SSE>(a, nf, st, "holdout sse")
+                                    : gemm<A_MMAJOR, 128, 128, 64, 32, EPI_MIS>(a, nf, st, "holdout mis");
+  if (rc) return rc;
+  const int mtiles = (int)((n_val + 127) / 128);
+  holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, metric, nullptr, nullptr,
+                                                             curves);
+  RP_LAUNCH_CHECK("holdout finish");
+  return RP_OK;
+}
+
+int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
+                    int64_t n_val, int d, int m, const double* W, int64_t ldw, int64_t w_fold_stride, int q, int nf,
+                    double* curves, void* work, void* stream) {
+  RP_REQUIRE(n_val >= 1, "rp_holdout_gram: empty validation set");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int N = q * m;
+  const int mtiles = (d + 127) / 128;
+  double* partial = (double*)work;
+  double* bc = partial + (size_t)nf * mtiles * N;
+  GemmArgs a = gemm_args();
+  a.M = d;
+  a.N = N;
+  a.K = d;
+  a.A = Gf;
+  a.lda = d;
+  a.strideA = g_stride;
+  a.B = W;
+  a.ldb = ldw;
+  a.strideB = w_fold_stride;
+  a.Y = W;
+  a.ldy = ldw;
+  a.strideY = w_fold_stride;
+  a.ycols = N;
+  a.partial = partial;
+  int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
+  if (rc) return rc;
+  holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
+  RP_LAUNCH_CHECK("holdout bc");
+  holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy, bc,
+                                                             curves);
+  RP_LAUNCH_CHECK("holdout gram finish");
+  return RP_OK;
+}
+
+int rp_select(const double* curves, int k, int q, int m, double* mean, int* best, void* stream) {
+  RP_REQUIRE(k >= 1 && q >= 1 && m >= 1, "rp_select: bad sizes");
+  select_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(curves, k, q, m, mean, best);
+  RP_LAUNCH_CHECK("select");
+  return RP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,256 @@
+// FP64 DMMA GEMM for the piCholesky CV path (sm_100a).
+//
+// C(M x N) = alpha * A(M x K) * B(K x N) + beta * C, batched over blockIdx.y.
+//   A layout: KMAJOR  -> A(m, k) at A[k * lda + m]   (X^T of a row-major X; a column-major L)
+//             MMAJOR  -> A(m, k) at A[m * lda + k]   (a row-major X_val)
+//   B layout: always  -> B(k, n) at B[k * ldb + n]
+//   C layout: column-major C(m, n) at C[n * ldc + m]
+// Epilogues:
+//   EPI_STORE    plain alpha/beta store (Gram blocks, X^T Y, Cholesky SYRK/TRSM updates)
+//   EPI_SSE      sum over rows of (acc - Y[m][n % ycols])^2   (direct RMSE hold-out)
+//   EPI_MIS      sum over rows of [sign(acc) != sign(Y)]       (direct MISCLASS hold-out)
+//   EPI_DOTB     sum over rows of acc * B2[m][n]                (Gram-form hold-out b^T G b)
+// The reduction epilogues never write C: they write one partial per (batch, m-tile, n) that a
+// second kernel sums over m-tiles in a fixed order (deterministic, no atomics).
+//
+// Tiling: 256 threads = 8 warps, CTA tile BM x BN, warp tile WM x WN, BK = 16, 3-stage cp.async
+// ring. Shared-memory strides are padded so both DMMA fragment reads are 2-wavefront
+// (conflict-free) loads: KMAJOR A / B rows padded to (width + 8) doubles, MMAJOR A rows to 20.
+#pragma once
+
+#include "rp_common.cuh"
+
+namespace rp {
+
+enum { EPI_STORE = 0, EPI_SSE = 1, EPI_MIS = 2, EPI_DOTB = 3 };
+enum { A_KMAJOR = 0, A_MMAJOR = 1 };
+
+struct GemmArgs {
+  int M, N, K;
+  const double* A;
+  int64_t lda, strideA;
+  const double* B;
+  int64_t ldb, strideB;
+  double* C;
+  int64_t ldc, strideC;
+  double alpha, beta;
+  int lower_only;  // square tiles only: compute tiles with tn <= tm (SYRK)
+  // reduction epilogues
+  const double* Y;  // EPI_SSE/EPI_MIS: Y(m, o) at Y[m * ldy + o];  EPI_DOTB: B2(m, n) at Y[m*ldy+n]
+  int64_t ldy, strideY;
+  int ycols;
+  double* partial;  // [batch][mtiles][N]
+};
+
+constexpr int GEMM_BK = 16;
+constexpr int GEMM_STAGES = 3;
+
+template <int AL, int BM, int BN>
+struct GemmSmem {
+  static constexpr int A_STRIDE = (AL == A_KMAJOR) ? (BM + 8) : (GEMM_BK + 4);
+  static constexpr int A_ELEMS = (AL == A_KMAJOR) ? GEMM_BK * A_STRIDE : BM * A_STRIDE;
+  static constexpr int B_STRIDE = BN + 8;
+  static constexpr int B_ELEMS = GEMM_BK * B_STRIDE;
+  static constexpr size_t BYTES = sizeof(double) * GEMM_STAGES * (A_ELEMS + B_ELEMS);
+};
+
+template <int AL, int BM, int BN, int WM, int WN, int EPI, bool VEC2>
+__global__ void __launch_bounds__(256) dgemm_kernel(GemmArgs p) {
+  constexpr int BK = GEMM_BK;
+  constexpr int MT = WM / 8, NT = WN / 8;
+  constexpr int WARPS_M = BM / WM;
+  static_assert((BM / WM) * (BN / WN) == 8, "8 warps");
+  using SM = GemmSmem<AL, BM, BN>;
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + GEMM_STAGES * SM::A_ELEMS;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int batch = blockIdx.y;
+
+  const int mtiles = (p.M + BM - 1) / BM;
+  int tm, tn;
+  if (p.lower_only) {
+    int lin = blockIdx.x;
+    tm = (int)((sqrt(8.0 * lin + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= lin) ++tm;
+    while (tm * (tm + 1) / 2 > lin) --tm;
+    tn = lin - tm * (tm + 1) / 2;
+  } else {
+    tm = blockIdx.x % mtiles;
+    tn = blockIdx.x / mtiles;
+  }
+  const int m0 = tm * BM, n0 = tn * BN;
+  const double* A = p.A + batch * p.strideA;
+  const double* B = p.B + batch * p.strideB;
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int ktiles = (p.K + BK - 1) / BK;
+
+  auto load_stage = [&](int kt, int st) {
+    const int k0 = kt * BK;
+    double* dA = sA + st * SM::A_ELEMS;
+    double* dB = sB + st * SM::B_ELEMS;
+    constexpr int V = VEC2 ? 2 : 1;
+    if (AL == A_KMAJOR) {
+      constexpr int PER_ROW = BM / V;
+      for (int c = tid; c < BK * PER_ROW; c += 256) {
+        int kk = c / PER_ROW, mm = (c % PER_ROW) * V;
+        int gk = k0 + kk, gm = m0 + mm;
+        bool ok = gk < p.K && gm < p.M;
+        const double* src = ok ? A + (int64_t)gk * p.lda + gm : A;
+        if (VEC2) cp_async16(dA + kk * SM::A_STRIDE + mm, src, ok);
+        else cp_async8(dA + kk * SM::A_STRIDE + mm, src, ok);
+      }
+    } else {
+      constexpr int PER_ROW = BK / V;
+      for (int c = tid; c < BM * PER_ROW; c += 256) {
+        int mm = c / PER_ROW, kk = (c % PER_ROW) * V;
+        int gk = k0 + kk, gm = m0 + mm;
+        bool ok = gk < p.K && gm < p.M;
+        const double* src = ok ? A + (int64_t)gm * p.lda + gk : A;
+        if (VEC2) cp_async16(dA + mm * SM::A_STRIDE + kk, src, ok);
+        else cp_async8(dA + mm * SM::A_STRIDE + kk, src, ok);
+      }
+    }
+    {
+      constexpr int PER_ROW = BN / V;
+      for (int c = tid; c < BK * PER_ROW; c += 256) {
+        int kk = c / PER_ROW, nn = (c % PER_ROW) * V;
+        int gk = k0 + kk, gn = n0 + nn;
+        bool ok = gk < p.K && gn < p.N;
+        const double* src = ok ? B + (int64_t)gk * p.ldb + gn : B;
+        if (VEC2) cp_async16(dB + kk * SM::B_STRIDE + nn, src, ok);
+        else cp_async8(dB + kk * SM::B_STRIDE + nn, src, ok);
+      }
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < GEMM_STAGES - 1; ++s) {
+    if (s < ktiles) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int st = kt % GEMM_STAGES;
+    {
+      int nk = kt + GEMM_STAGES - 1;
+      if (nk < ktiles) load_stage(nk, nk % GEMM_STAGES);
+      cp_async_commit();
+    }
+    cp_async_wait<GEMM_STAGES - 1>();
+    __syncthreads();
+    const double* a_s = sA + st * SM::A_ELEMS;
+    const double* b_s = sB + st * SM::B_ELEMS;
+#pragma unroll
+    for (int ks = 0; ks < BK / 4; ++ks) {
+      const int k = ks * 4 + t;
+      double af[MT], bf[NT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        int row = wm * WM + i * 8 + g;
+        af[i] = (AL == A_KMAJOR) ? a_s[k * SM::A_STRIDE + row] : a_s[row * SM::A_STRIDE + k];
+      }
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = b_s[k * SM::B_STRIDE + wn * WN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  if (EPI == EPI_STORE) {
+    double* C = p.C + batch * p.strideC;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      int row = m0 + wm * WM + i * 8 + g;
+      if (row >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int col = n0 + wn * WN + j * 8 + 2 * t + h;
+          if (col >= p.N) continue;
+          double* c = C + (int64_t)col * p.ldc + row;
+          double v = p.alpha * acc[i][j][h];
+          if (p.beta != 0.0) v = fma(p.beta, *c, v);
+          *c = v;
+        }
+      }
+    }
+  } else {
+    // Row-reduction epilogues: each lane sums its rows for each of its columns, then the 8
+    // lanes sharing t (same columns) reduce over g, then warps sharing wn reduce via smem.
+    const double* Yb = p.Y + batch * p.strideY;
+    double colsum[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) colsum[j][0] = colsum[j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      int row = m0 + wm * WM + i * 8 + g;
+      if (row >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int col = n0 + wn * WN + j * 8 + 2 * t + h;
+          if (col >= p.N) continue;
+          double v;
+          if (EPI == EPI_SSE) {
+            double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
+            double e = acc[i][j][h] - y;
+            v = e * e;
+          } else if (EPI == EPI_MIS) {
+            double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
+            double s_pred = acc[i][j][h] >= 0.0 ? 1.0 : -1.0;
+            double s_y = (y > 0.0) ? 1.0 : ((y < 0.0) ? -1.0 : 0.0);
+            v = (s_pred != s_y) ? 1.0 : 0.0;
+          } else {
+            v = acc[i][j][h] * Yb[(int64_t)row * p.ldy + col];
+          }
+          colsum[j][h] += v;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = colsum[j][h];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        colsum[j][h] = v;
+      }
+    __syncthreads();
+    double* red = smem;  // [WARPS_M][BN]
+    if (g == 0) {
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) red[wm * BN + wn * WN + j * 8 + 2 * t + h] = colsum[j][h];
+    }
+    __syncthreads();
+    for (int c = tid; c < BN; c += 256) {
+      int col = n0 + c;
+      if (col >= p.N) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < WARPS_M; ++w) s += red[w * BN + c];
+      p.partial[((int64_t)batch * mtiles + tm) * p.N + col] = s;
+    }
+  }
+}
+
+}  // namespace rp

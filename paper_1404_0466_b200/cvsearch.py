@@ -1,0 +1,273 @@
+"""Cross-validated selection of the ridge parameter on the B200
+(drop-in for the hot path of ridgepath/cvsearch.py).
+
+``grid_search_pichol`` (cvsearch.py:206-243) keeps the reference's signature,
+validation and report (CvReport with per-lambda fold-mean errors keyed by
+float(lambda), first-argmin selection, per-fold CSV rows and phase timings).
+The whole sweep -- per-fold Hessians, the s x k sampled-lambda Choleskys, the
+polynomial fit, the fused evaluate+solve for all q lambdas and the hold-out
+errors -- runs on the device through ``engine.PicholEngine``; only the q x m
+curve matrix and the selection come back to the host.
+
+Multi-output generalization: ``Dataset.y`` may be (n, m). The per-output fold
+curves are in ``CvReport.curves`` (k, q, m) with per-output selections in
+``best_index``; ``per_lambda_error``/``best_lambda``/``best_error`` then
+describe the mean over outputs. For 1-D y the report matches the reference.
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _dev, _ops, pichol, trivec
+from .engine import MISCLASS, RMSE, PicholEngine
+from .errors import DimensionMismatch, EmptyValidationSet, InvalidThreshold, SingularInterpolant, UsageError
+
+METRICS = (RMSE, MISCLASS)
+PHASES = ("factorize", "vec", "fit", "interp", "solve", "predict")
+THREADS_ENV = "RIDGEPATH_THREADS"
+
+
+@dataclass
+class Dataset:
+    """Full design and labels; fold plans slice it into train/validation."""
+
+    X: np.ndarray
+    y: np.ndarray
+
+
+@dataclass
+class LambdaGrid:
+    lo: float
+    hi: float
+    q: int
+    values: np.ndarray
+
+
+def make_grid(lo, hi, q):
+    """q log-spaced values from lo to hi inclusive (cvsearch.py:55-66)."""
+    if not (0 < lo < hi):
+        raise UsageError(f"need 0 < lo < hi, got lo={lo}, hi={hi}")
+    if q < 1:
+        raise UsageError(f"grid size must be >= 1, got q={q}")
+    if q == 1:
+        values = np.array([lo])
+    else:
+        values = np.logspace(np.log10(lo), np.log10(hi), q)
+        values[0], values[-1] = lo, hi
+    return LambdaGrid(lo=lo, hi=hi, q=q, values=values)
+
+
+@dataclass
+class FoldPlan:
+    k: int
+    assignments: np.ndarray
+    seed: int
+
+
+def make_folds(n, k, seed, labels=None):
+    """Seeded fold assignment; stratified when labels are +/-1 (cvsearch.py:76-92)."""
+    if k < 2:
+        raise UsageError(f"need k >= 2 folds, got {k}")
+    if k > n:
+        raise UsageError(f"cannot split {n} samples into {k} nonempty folds")
+    rng = np.random.default_rng(seed)
+    assignments = np.empty(n, dtype=np.int64)
+    if labels is not None and set(np.unique(labels)) <= {-1.0, 1.0}:
+        for cls in (-1.0, 1.0):
+            idx = np.flatnonzero(np.asarray(labels) == cls)
+            idx = rng.permutation(idx)
+            assignments[idx] = np.arange(idx.size) % k
+    else:
+        perm = rng.permutation(n)
+        assignments[perm] = np.arange(n) % k
+    return FoldPlan(k=k, assignments=assignments, seed=seed)
+
+
+def contiguous_folds(n, k, seed=0):
+    """BASELINE.json folds: contiguous blocks of n // k rows."""
+    return FoldPlan(k=k, assignments=np.arange(n) // (n // k), seed=seed)
+
+
+@dataclass
+class CvReport:
+    method: str
+    per_lambda_error: dict
+    best_lambda: float
+    best_error: float
+    timings: dict
+    rows: list = field(default_factory=list)
+    wall_seconds: float = 0.0
+    curves: np.ndarray | None = None  # (k, q, m) per-fold, per-output errors
+    best_index: np.ndarray | None = None  # (m,) per-output first-argmin index
+
+
+def holdout_error(theta, X_val, y_val, metric=RMSE):
+    """Validation error of one solution (cvsearch.py:106-123), computed on the device."""
+    X_val = np.asarray(X_val, dtype=float)
+    y_val = np.asarray(y_val, dtype=float).reshape(-1)
+    if X_val.shape[0] == 0:
+        raise EmptyValidationSet("validation set is empty")
+    if X_val.shape[0] != y_val.shape[0]:
+        raise DimensionMismatch(f"{X_val.shape[0]} rows vs {y_val.shape[0]} targets")
+    if metric not in METRICS:
+        raise UsageError(f"unknown metric {metric!r}")
+    return float(_ops.holdout(np.asarray(theta, dtype=float).reshape(-1), X_val, y_val, metric)[0])
+
+
+def resolve_threads(threads=None):
+    """Thread count from the argument, RIDGEPATH_THREADS, or 1 (cvsearch.py:126-134).
+
+    Accepted for API compatibility; the device sweep does not use host threads."""
+    if threads is None:
+        threads = os.environ.get(THREADS_ENV, "1")
+    try:
+        threads = int(threads)
+    except ValueError as e:
+        raise UsageError(f"bad thread count {threads!r}") from e
+    return max(1, threads)
+
+
+def _zero_timings():
+    return dict.fromkeys(PHASES, 0.0)
+
+
+def fold_order(folds, n):
+    """Stable grouping of rows by fold (keeps the reference's row order inside each fold,
+    cvsearch.py:145-147). Returns (row order, rows per fold)."""
+    a = np.asarray(folds.assignments)
+    if a.shape[0] != n:
+        raise DimensionMismatch(f"fold plan covers {a.shape[0]} rows, data has {n}")
+    counts = np.bincount(a, minlength=folds.k)[: folds.k]
+    if np.any(a < 0) or np.any(a >= folds.k):
+        raise UsageError("fold assignments outside [0, k)")
+    if np.any(counts == 0):
+        raise EmptyValidationSet("validation set is empty")
+    if np.all(a[:-1] <= a[1:]):
+        return None, counts
+    return np.argsort(a, kind="stable"), counts
+
+
+def _merge(method, grid_values, curves, times_per_fold, wall):
+    """Fold mean + first argmin + CSV rows (cvsearch.py:154-175). curves: (k, q, m)."""
+    k, q, m = curves.shape
+    errs_all = np.mean(curves, axis=0)  # (q, m)
+    errs = errs_all[:, 0] if m == 1 else np.mean(errs_all, axis=1)
+    timings = _zero_timings()
+    rows = []
+    for i in range(k):
+        for phase in PHASES:
+            timings[phase] += times_per_fold[phase]
+        fold_errs = curves[i, :, 0] if m == 1 else np.mean(curves[i], axis=1)
+        for lam, e in zip(grid_values, fold_errs):
+            rows.append({"fold": i, "lambda": float(lam), "error": float(e), **times_per_fold})
+    best_idx = int(np.argmin(errs))
+    for lam, e in zip(grid_values, errs):
+        rows.append({"fold": -1, "lambda": float(lam), "error": float(e), **_zero_timings()})
+    return CvReport(
+        method=method,
+        per_lambda_error={float(l): float(e) for l, e in zip(grid_values, errs)},
+        best_lambda=float(grid_values[best_idx]),
+        best_error=float(errs[best_idx]),
+        timings=timings,
+        rows=rows,
+        wall_seconds=wall,
+        curves=curves,
+        best_index=np.argmin(errs_all, axis=0),
+    )
+
+
+def prepare_design(p, folds):
+    """Host arrays grouped by fold (no copy for contiguous plans): (X, Y (n, m), block rows)."""
+    X = np.asarray(p.X, dtype=float)
+    y = np.asarray(p.y, dtype=float)
+    Y = y.reshape(-1, 1) if y.ndim == 1 else y
+    if X.ndim != 2 or X.shape[0] != Y.shape[0]:
+        raise DimensionMismatch(f"{X.shape[0]} rows vs {Y.shape[0]} targets")
+    order, counts = fold_order(folds, X.shape[0])
+    if order is not None:
+        X, Y = X[order], Y[order]
+    return np.ascontiguousarray(X), np.ascontiguousarray(Y), counts
+
+
+def grid_search_pichol(
+    p,
+    grid,
+    folds,
+    metric=RMSE,
+    g=4,
+    r=2,
+    layout_kind=trivec.RECURSIVE,
+    h0=64,
+    raw_monomials=False,
+    threads=None,
+    holdout="auto",
+):
+    """Fit the factor polynomials per fold, then sweep the grid on the device (cvsearch.py:206-243).
+
+    ``layout_kind``/``h0`` are validated for compatibility; the device always packs
+    factors in the tile layout, which gives the same fitted values (the fit is
+    per entry, so it is layout independent, tests/test_pichol.py:73-83).
+    """
+    if g > grid.q:
+        raise UsageError(f"cannot draw g={g} samples from a grid of {grid.q}")
+    if metric not in METRICS:
+        raise UsageError(f"unknown metric {metric!r}")
+    threads = resolve_threads(threads)
+    t_start = time.perf_counter()
+    sample_lams = grid.values[pichol.sample_indices(grid.q, g)]
+    lams, V, cond_raw, t_scale, t_shift, Pm = _fit_basis_checked(sample_lams, r, raw_monomials)
+    X, Y, counts = prepare_design(p, folds)
+    n, d = X.shape
+    if layout_kind not in trivec.ALL_KINDS:
+        raise DimensionMismatch(f"unknown layout kind {layout_kind!r}")
+    if layout_kind == trivec.RECURSIVE and h0 < 1:
+        raise InvalidThreshold(f"recursion threshold must be >= 1, got {h0}")
+    m = Y.shape[1]
+    eng = PicholEngine(counts, d, m, grid.q, lams.shape[0], r, metric=metric, holdout=holdout)
+    dX, dY = _dev.to_dev(X), _dev.to_dev(Y)
+    tvals = t_scale * np.asarray(grid.values, dtype=float) + t_shift
+    timings = {}
+    curves_dev, _, _ = eng.sweep(dX, dY, lams, Pm, V, tvals, timings=timings)
+    bad = eng.check_numerics(lams)
+    if bad is not None:
+        f, j = bad
+        raise SingularInterpolant(f"interpolated factor is singular at lambda={grid.values[j]} (fold {f})")
+    curves = curves_dev.cpu().numpy()
+    k = folds.k
+    per_fold = _zero_timings()
+    per_fold["factorize"] = timings.get("factorize", 0.0) / k
+    per_fold["fit"] = timings.get("fit", 0.0) / k
+    per_fold["interp"] = timings.get("interp", 0.0) / k
+    per_fold["predict"] = (timings.get("predict_local", 0.0) + timings.get("predict", 0.0)) / k
+    return _merge("pichol", grid.values, curves, per_fold, time.perf_counter() - t_start)
+
+
+def _fit_basis_checked(sample_lams, r, raw_monomials):
+    from .errors import DegenerateSamples, InsufficientSamples
+
+    lams = np.asarray(sample_lams, dtype=float)
+    if lams.shape[0] <= r:
+        raise InsufficientSamples(f"need more samples than the degree: g={lams.shape[0]}, r={r}")
+    if np.unique(lams).shape[0] != lams.shape[0]:
+        raise DegenerateSamples("sample lambdas must be distinct")
+    if np.any(lams <= 0):
+        raise DegenerateSamples("sample lambdas must be positive")
+    return pichol.fit_basis(lams, r, raw_monomials)
+
+
+CSV_HEADER = "method,fold,lambda,error," + ",".join(f"t_{ph}" for ph in PHASES)
+
+
+def report_csv_lines(report):
+    """Render a CvReport as CSV lines, header first (cvsearch.py:429-444)."""
+    lines = [CSV_HEADER]
+    for row in report.rows:
+        cells = [report.method, str(row["fold"]), f"{row['lambda']:.17g}", f"{row['error']:.17g}"]
+        cells += [f"{row[ph]:.6g}" for ph in PHASES]
+        lines.append(",".join(cells))
+    return lines
