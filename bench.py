@@ -1,0 +1,363 @@
+"""Benchmark of the piCholesky CV sweep (BASELINE.json headline: c4, d=4096).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+A step is one full k-fold x q-lambda sweep (per-fold Hessians -> s sampled
+Choleskys -> polynomial fit -> fused eval+solve for all q lambdas -> hold-out
+errors -> fold mean + argmin) on the seeded synthetic c4 data with X resident
+in HBM (3.3 GB > 126 MB L2, so every step streams its inputs from HBM; no L2
+flush needed). value = k*q fold-lambda evals / step time (max over ranks).
+e2e = the same metric through the public API (cvsearch.CvSession.run) with
+pinned host X/Y copied in and curves + selection read back every step.
+
+Under torchrun (N > 1) folds are sharded f -> rank f % N; Gram blocks and
+curves are all-gathered over NCCL (paper_1404_0466_b200/dist.py).
+
+--impl reference times the CPU oracle port (oracle/pichol_oracle.py, a line-by-
+line restatement of the reference package, which is pure Python) on the host
+cores, on a bounded sample of the same workload (one fold's setup + a few
+lambdas per step, extrapolated to the full sweep).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fold-lambda CV evals/sec at d=4096 (1/2/4/8 B200); HBM/FP64 roofline fraction"
+UNIT = "fold-lambda evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--holdout", default="auto", choices=["auto", "gram", "direct"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-lams", type=int, default=4, help="lambdas timed per CPU sample")
+    ap.add_argument("--profile-stages", action="store_true", help="print per-stage timings to stderr")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    """Roofline denominators: driver-measured HBM copy; FP64 DMMA measured by tools/fp64_peaks.cu."""
+    out = {"hbm_gbs": 6552.0, "hbm_src": "fallback", "fp64_tflops": 37.0, "fp64_src": "fallback"}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            out["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
+            out["hbm_src"] = "MEASURED_PEAKS.json"
+    p = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            vals = [json.loads(line) for line in f if line.strip()]
+        out["fp64_tflops"] = max(v["dmma884_tflops_b4"] for v in vals)
+        out["fp64_src"] = "profiles/r01_fp64_peaks.json (mma.sync.m8n8k4.f64, burst)"
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = sorted(sm)[len(sm) // 4:] or sm  # drop idle ramp samples
+        return {"sm_mhz": float(np.median(loaded)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle (reference arm + cpu_baseline)
+
+
+def cpu_sample(cfg, X, Y, fold, n_lam):
+    """Time the oracle port on one fold: setup (assemble + s Choleskys + fit) and n_lam lambdas.
+    Returns (t_setup, t_per_lambda)."""
+    from oracle import pichol_oracle as orc
+
+    k, q = cfg.k, cfg.q
+    grid = orc.make_grid(cfg.lo, cfg.hi, q)
+    assign = np.arange(cfg.n) // (cfg.n // k)
+    val = assign == fold
+    t0 = time.perf_counter()
+    H, G = orc.assemble(X[~val], Y[~val])
+    model = orc.fit(H, grid[orc.sample_indices(q, cfg.s)], cfg.r)
+    t1 = time.perf_counter()
+    lam_idx = np.linspace(0, q - 1, n_lam).round().astype(int)
+    for li in lam_idx:
+        B = orc.solve_interp(model, G, grid[li])
+        orc.holdout_error(B, X[val], Y[val])
+    t2 = time.perf_counter()
+    return t1 - t0, (t2 - t1) / n_lam
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, world, rank):
+    if rank != 0:
+        return
+    from paper_1404_0466_b200 import configs
+
+    X, Y = configs.generate(cfg)
+    step_times, setups, lams = [], [], []
+    for i in range(args.warmup + args.steps):
+        fold = i % cfg.k
+        t_setup, t_lam = cpu_sample(cfg, X, Y, fold, args.cpu_lams)
+        if i >= args.warmup:
+            setups.append(t_setup)
+            lams.append(t_lam)
+            step_times.append(t_setup + cfg.q * t_lam)  # one fold's full lambda sweep, extrapolated
+    per_fold = float(np.mean(step_times))
+    value = cfg.q / per_fold  # k*q evals / (k * per-fold time)
+    sample = (f"per step: fold i%k of {cfg.name} (assemble + {cfg.s} Choleskys + fit) + {args.cpu_lams} of "
+              f"{cfg.q} lambdas, extrapolated linearly to all {cfg.q} lambdas and k={cfg.k} folds")
+    out = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": per_fold * cfg.k * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_1404_0466_b200/configs.py)",
+        "config": config_dict(cfg, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample,
+                         "t_setup_s": float(np.mean(setups)), "t_lambda_s": float(np.mean(lams))},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def config_dict(cfg, world):
+    return {"workload": f"{cfg.name}: piCholesky {cfg.k}-fold CV sweep", "n": cfg.n, "d": cfg.d, "outputs": cfg.m,
+            "folds": cfg.k, "sampled_lambdas": cfg.s, "degree": cfg.r, "grid": cfg.q,
+            "lambda_range": [cfg.lo, cfg.hi], "parallelism": f"fold-sharded x{world}",
+            "l2": "inputs (X 3.3 GB at c4) exceed the 126 MB L2; no flush"}
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    from paper_1404_0466_b200 import configs
+
+    cfg = configs.CONFIGS[args.config]
+    if world > 1:
+        import torch.distributed as dist
+
+        if args.impl == "reference":
+            if rank != 0:
+                return
+        else:
+            import torch
+
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        return
+    run_ours(args, cfg, world, rank, local)
+
+
+def run_ours(args, cfg, world, rank, local):
+    import torch
+
+    from paper_1404_0466_b200 import _lib, configs, cvsearch, dist
+    from paper_1404_0466_b200.engine import solve_bytes, sweep_flops
+
+    torch.cuda.set_device(local)
+    _lib.require_cuda()
+    X, Y = configs.generate(cfg)
+    grid = configs.grid_values(cfg)
+    shard = dist.Shard(rank, world, cfg.k)
+    sess = cvsearch.CvSession([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, grid, g=cfg.s, r=cfg.r,
+                              holdout=args.holdout, shard=shard)
+    Xp = torch.from_numpy(X).pin_memory()
+    Yp = torch.from_numpy(Y).pin_memory()
+    sess.upload(Xp, Yp)
+    torch.cuda.synchronize()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(args.warmup, 0)):
+        sess.sweep()
+    torch.cuda.synchronize()
+
+    # ---- device-timed region: K sweeps with X resident
+    stage_t = {}
+    launches0 = _lib.query("rp_launch_count")
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            sess.sweep()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    launches = _lib.query("rp_launch_count") - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = cfg.k * cfg.q / (ms / 1e3)
+
+    # ---- per-stage breakdown (separate pass, events between stages)
+    for _ in range(2):
+        st = {}
+        sess.sweep(timings=st)
+    stage_t = st
+
+    # ---- end to end through the public API (pinned host in, curves + argmin out)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(2, min(args.steps, 3))
+    sess.run(Xp, Yp)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        curves, best = sess.run(Xp, Yp)
+    t_e2e = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([t_e2e], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(t.item())
+    e2e_value = cfg.k * cfg.q / t_e2e
+
+    # ---- roofline of the dominant stage
+    pk = peaks()
+    flops = sweep_flops(cfg.k, cfg.n, cfg.d, cfg.m, cfg.q, cfg.s, cfg.r, nf=len(shard.local_folds),
+                        holdout=sess.engine.holdout)
+    stage_map = {"assemble": "gram", "factorize": "factorize", "fit": "fit", "interp": "solve",
+                 "predict_local": "holdout"}
+    stages = {}
+    for name, key in stage_map.items():
+        if name in stage_t:
+            ts = stage_t[name]
+            stages[key] = {"ms": ts * 1e3, "tflops": flops[key] / ts / 1e12,
+                           "frac_fp64": flops[key] / ts / 1e12 / pk["fp64_tflops"]}
+    dom = max(stages, key=lambda s: stages[s]["ms"])
+    nf = len(shard.local_folds)
+    roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
+            "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": None,
+            "peak_src": pk["fp64_src"], "algorithmic_flops": flops[dom] }
+    stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9 if "solve" in stages else None
+
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_1404_0466_b200/configs.py)",
+        "config": config_dict(cfg, world),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sess.h2d_bytes,
+                "d2h_bytes_per_step": sess.d2h_bytes, "ms_per_step": t_e2e * 1e3},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "roofline": roof,
+        "stages": stages,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        t_setup, t_lam = cpu_sample(cfg, X, Y, 0, args.cpu_lams)
+        cpu_val = cfg.q / (t_setup + cfg.q * t_lam)
+        out["cpu_baseline"] = {
+            "value": cpu_val, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+            "sample": f"fold 0 of {cfg.name}: assemble + {cfg.s} Choleskys + fit + {args.cpu_lams} of {cfg.q} "
+                      f"lambdas on the oracle port, extrapolated to the full sweep",
+            "t_setup_s": t_setup, "t_lambda_s": t_lam}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

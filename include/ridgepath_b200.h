@@ -47,6 +47,8 @@ extern "C" {
 
 int rp_version(void);
 const char* rp_last_error(void);
+/* Number of kernels this library has launched in the process (evidence for bench.py). */
+long long rp_launch_count(void);
 
 /* Number of 64 x 64 tiles of the packed lower triangle of order d. */
 int64_t rp_tile_count(int d);

@@ -32,6 +32,7 @@ _sz = ctypes.c_size_t
 SIGNATURES = {
     "rp_version": (_i, []),
     "rp_last_error": (ctypes.c_char_p, []),
+    "rp_launch_count": (ctypes.c_longlong, []),
     "rp_tile_count": (_i64, [_i]),
     "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp]),
     "rp_col_sumsq": (_i, [_vp, _i64, _i64, _i, _i, _vp, _vp]),

@@ -54,6 +54,7 @@ RP_DEVINL void cp_async_wait() {
 // ---- host-side error plumbing shared by the C-ABI translation units ----
 namespace rp {
 int set_error(int code, const char* fmt, ...);  // records rp_last_error(), returns code
+void count_launch();                             // rp_launch_count() bookkeeping
 inline int cuda_status(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return RP_OK;
   return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
@@ -62,6 +63,7 @@ inline int cuda_status(cudaError_t e, const char* where) {
 
 #define RP_LAUNCH_CHECK(where)                          \
   do {                                                  \
+    rp::count_launch();                                 \
     cudaError_t _e = cudaGetLastError();                \
     if (_e != cudaSuccess) return rp::cuda_status(_e, where); \
   } while (0)

@@ -1,6 +1,7 @@
 // C-ABI entry points for the piCholesky CV path (everything except the fused eval+solve,
 // which lives in rp_solve.cu). See include/ridgepath_b200.h for the contract and the
 // reference routine each entry point replaces.
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -24,6 +25,9 @@ int set_error(int code, const char* fmt, ...) {
   g_last_error = buf;
   return code;
 }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -417,6 +421,8 @@ static inline int grid1d(int64_t n, int b = 256) { return (int)((n + b - 1) / b)
 extern "C" {
 
 int rp_version(void) { return 1; }
+
+long long rp_launch_count(void) { return rp::g_launches.load(); }
 
 const char* rp_last_error(void) { return rp::g_last_error.c_str(); }
 

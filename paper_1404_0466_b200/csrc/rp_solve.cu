@@ -1,272 +1,31 @@
-// (5) Fused evaluate + solve: for every local fold f and every grid lambda_j,
-//       W_f(:, j) = (L_f(t_j) L_f(t_j)^T)^{-1} rhs_f,   L_f(t) = sum_p theta_{f,p} t^p,
-// without ever materializing L_f(t_j). Replaces pichol.eval_vector (pichol.py:143-151)
-// + trivec.unvectorize (trivec.py:150-162) + the singular check (ridge.py:88-89) +
-// linalg.solve_chol (linalg.py:104-128), once per lambda in the reference's q-lambda loop
-// (cvsearch.py:232-239).
-//
-// Design (B200, FP64 = one DMMA/DFMA datapath, 64 MAC/clk/SM):
-//  * One CTA owns a chain (fold f, chunk of <= 16 lambdas) and runs the blocked, left-looking
-//    forward substitution over 64-row tile rows (kernel BWD=false) and, in a second launch, the
-//    backward substitution with the transposed tiles (BWD=true). No inter-CTA dependencies,
-//    so the result is deterministic and independent of the grid.
-//  * Off-diagonal tiles are streamed as 16-column (fwd) / 16-row (bwd) slabs through a 3-stage
-//    cp.async ring together with the matching 16 rows of the already-solved W.
-//  * Per slab each warp owns 8 output rows. For each k-step it loads the P coefficient planes
-//    of its A fragment once, evaluates L(t_l) for every lambda of the chunk with Horner in
-//    registers (DFMA), and feeds it to mma.m8n8k4.f64 against W_J(lambda) (N = 8 outputs per
-//    DMMA). The m % 8 leftover outputs are done with DFMA on the same evaluated fragment and
-//    reduced across the 4 k-lanes at the end of the row (no N padding waste).
-//  * The 64 x 64 diagonal tile is solved in shared memory, one thread per (lambda, output)
-//    column, reading its coefficients through the read-only path (uniform addresses ->
-//    broadcast). The diagonal pass also raises the SingularInterpolant flag.
-#include "rp_common.cuh"
+// (5) Fused evaluate + solve: host dispatch of rp_eval_solve and the generic (runtime P and
+// chunk size) kernel instantiations. The kernel itself is in rp_solve.cuh; the specialised
+// (compile-time P and chunk) instantiations used by the BASELINE configs are in rp_solve_fast.cu.
+#include "rp_solve.cuh"
 #include "../../include/ridgepath_b200.h"
 
-namespace rp {
+using namespace rp;
 
-constexpr int SOLVE_LC = 16;     // max lambdas per CTA
-constexpr int SOLVE_PMAX = 5;    // max polynomial planes (degree <= 4)
-constexpr int SOLVE_STAGES = 3;
-constexpr int FWD_SLAB = 16 * 68;   // per plane: 16 columns x 64 rows (stride 68)
-constexpr int BWD_SLAB = 64 * 20;   // per plane: 64 columns x 16 rows (stride 20)
-
-struct SolveArgs {
-  const double* theta;
-  int64_t theta_fold_stride;
-  const double* rhs;
-  int64_t rhs_fold_stride;
-  double* W;
-  int64_t ldw, w_fold_stride;
-  const double* tvals;
-  int* flags;
-  int q, m, d, nt, P, lam_per_cta, chunks, S;
-};
-
-RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
-
-template <int NT, int REM, bool BWD>
-__global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
-  constexpr int LC = SOLVE_LC;
-  constexpr int REMA = REM > 0 ? REM : 1;
-  constexpr int SLAB = BWD ? BWD_SLAB : FWD_SLAB;
-  extern __shared__ __align__(16) double smem[];
-  const int P = a.P, S = a.S, m = a.m;
-  const int stageT = P * SLAB;
-  const int stageW = 16 * S;
-  double* sT = smem;
-  double* sW = smem + SOLVE_STAGES * stageT;
-  double* sR = sW + SOLVE_STAGES * stageW;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int fold = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
-  const int l0 = chunk * a.lam_per_cta;
-  const int nl = min(a.lam_per_cta, a.q - l0);
-  if (nl <= 0) return;
-  const double* theta = a.theta + fold * a.theta_fold_stride;
-  double* W = a.W + fold * a.w_fold_stride;
-  const int cw = nl * m;            // valid chunk columns
-  const int cpairs = (cw + 1) >> 1;  // 16-byte copies per W row
-  const int64_t wcol0 = (int64_t)l0 * m;
-
-  double tl[LC];
-#pragma unroll
-  for (int l = 0; l < LC; ++l) tl[l] = (l < nl) ? a.tvals[l0 + l] : 0.0;
-
-  double acc[LC][NT > 0 ? NT : 1][2];
-  double accx[LC][REMA];
-
-  for (int step = 0; step < a.nt; ++step) {
-    const int I = BWD ? (a.nt - 1 - step) : step;
-    const int nslab = 4 * (BWD ? (a.nt - 1 - I) : I);
-#pragma unroll
-    for (int l = 0; l < LC; ++l) {
-#pragma unroll
-      for (int j = 0; j < (NT > 0 ? NT : 1); ++j) acc[l][j][0] = acc[l][j][1] = 0.0;
-#pragma unroll
-      for (int c = 0; c < REMA; ++c) accx[l][c] = 0.0;
-    }
-
-    auto issue = [&](int s) {
-      if (s < nslab) {
-        const int st = s % SOLVE_STAGES;
-        const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
-        const int kq = s & 3;
-        const double* tile = theta + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * 4096;
-        double* dT = sT + st * stageT;
-        for (int c = tid; c < P * 512; c += 256) {
-          const int p = c >> 9, e = c & 511;
-          if (!BWD) {
-            const int kk = e >> 5, i2 = (e & 31) * 2;  // column kq*16+kk, rows i2, i2+1
-            cp_async16(dT + p * FWD_SLAB + kk * 68 + i2, tile + p * 4096 + (kq * 16 + kk) * 64 + i2, true);
-          } else {
-            const int i = e >> 3, k2 = (e & 7) * 2;  // column i, rows kq*16+k2, +1
-            cp_async16(dT + p * BWD_SLAB + i * 20 + k2, tile + p * 4096 + i * 64 + kq * 16 + k2, true);
-          }
-        }
-        double* dW = sW + st * stageW;
-        const double* src = W + (int64_t)(J * 64 + kq * 16) * a.ldw + wcol0;
-        for (int c = tid; c < 16 * cpairs; c += 256) {
-          const int kk = c / cpairs, c2 = (c - kk * cpairs) * 2;
-          cp_async16(dW + kk * S + c2, src + (int64_t)kk * a.ldw + c2, true);
-        }
-      }
-      cp_async_commit();
-    };
-
-    issue(0);
-    issue(1);
-    for (int s = 0; s < nslab; ++s) {
-      issue(s + 2);
-      cp_async_wait<2>();
-      __syncthreads();
-      const double* T = sT + (s % SOLVE_STAGES) * stageT;
-      const double* Wb = sW + (s % SOLVE_STAGES) * stageW;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int k = ks * 4 + t;
-        double th[SOLVE_PMAX];
-#pragma unroll
-        for (int p = 0; p < SOLVE_PMAX; ++p) {
-          if (p < P) th[p] = BWD ? T[p * BWD_SLAB + (warp * 8 + g) * 20 + k] : T[p * FWD_SLAB + k * 68 + warp * 8 + g];
-        }
-        const double* wrow = Wb + k * S;
-#pragma unroll
-        for (int l = 0; l < LC; ++l) {
-          if (l < nl) {
-            // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
-            double av = 0.0;
-#pragma unroll
-            for (int p = SOLVE_PMAX - 1; p >= 0; --p) {
-              if (p < P) av = (p == P - 1) ? th[p] : fma(av, tl[l], th[p]);
-            }
-#pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              double b = wrow[l * m + j * 8 + g];
-              dmma884(acc[l][j][0], acc[l][j][1], av, b);
-            }
-#pragma unroll
-            for (int c = 0; c < REM; ++c) accx[l][c] = fma(av, wrow[l * m + NT * 8 + c], accx[l][c]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-
-    // ---- diagonal tile: R = base - acc into sR, then triangular solve per column ----
-    const int rowI = I * 64;
-#pragma unroll
-    for (int l = 0; l < LC; ++l) {
-      if (l < nl) {
-#pragma unroll
-        for (int c = 0; c < REM; ++c) {
-          double v = accx[l][c];
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          accx[l][c] = v;
-        }
-        const int i = warp * 8 + g;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = j * 8 + 2 * t + h;
-            double base = BWD ? W[(int64_t)(rowI + i) * a.ldw + wcol0 + l * m + col]
-                              : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + i) * m + col];
-            sR[i * S + l * m + col] = base - acc[l][j][h];
-          }
-        }
-        if (t == 0) {
-#pragma unroll
-          for (int c = 0; c < REM; ++c) {
-            const int col = NT * 8 + c;
-            double base = BWD ? W[(int64_t)(rowI + i) * a.ldw + wcol0 + l * m + col]
-                              : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + i) * m + col];
-            sR[i * S + l * m + col] = base - accx[l][c];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tid < cw) {
-      const int l = tid / m, col = tid - (tid / m) * m;
-      const double tv = a.tvals[l0 + l];
-      const double* th = theta + (int64_t)tile_index(I, I) * P * 4096;
-      double* x = sR + l * m + col;
-      auto horner = [&](int off) {
-        double v = __ldg(th + (P - 1) * 4096 + off);
-        for (int p = P - 2; p >= 0; --p) v = fma(v, tv, __ldg(th + p * 4096 + off));
-        return v;
-      };
-      if (!BWD) {
-        bool singular = false;
-        for (int i = 0; i < 64; ++i) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int k = 0;
-          for (; k + 4 <= i; k += 4) {
-            s0 = fma(horner((k + 0) * 64 + i), x[(k + 0) * S], s0);
-            s1 = fma(horner((k + 1) * 64 + i), x[(k + 1) * S], s1);
-            s2 = fma(horner((k + 2) * 64 + i), x[(k + 2) * S], s2);
-            s3 = fma(horner((k + 3) * 64 + i), x[(k + 3) * S], s3);
-          }
-          for (; k < i; ++k) s0 = fma(horner(k * 64 + i), x[k * S], s0);
-          const double lii = horner(i * 64 + i);
-          if (rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
-          x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
-        }
-        if (singular && col == 0) a.flags[fold * a.q + l0 + l] = 1;
-      } else {
-        for (int i = 63; i >= 0; --i) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int k = i + 1;
-          for (; k + 4 <= 64; k += 4) {
-            s0 = fma(horner(i * 64 + k + 0), x[(k + 0) * S], s0);
-            s1 = fma(horner(i * 64 + k + 1), x[(k + 1) * S], s1);
-            s2 = fma(horner(i * 64 + k + 2), x[(k + 2) * S], s2);
-            s3 = fma(horner(i * 64 + k + 3), x[(k + 3) * S], s3);
-          }
-          for (; k < 64; ++k) s0 = fma(horner(i * 64 + k), x[k * S], s0);
-          const double lii = horner(i * 64 + i);
-          x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
-        }
-      }
-    }
-    __syncthreads();
-    for (int e = tid; e < 64 * cw; e += 256) {
-      const int i = e / cw, c = e - (e / cw) * cw;
-      W[(int64_t)(rowI + i) * a.ldw + wcol0 + c] = sR[i * S + c];
-    }
-    __syncthreads();
+static int launch_generic(int m, const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
+  switch (m) {
+    case 1: return launch_solve<0, 1, 0, 0>(a, grid, smem, st);
+    case 2: return launch_solve<0, 2, 0, 0>(a, grid, smem, st);
+    case 3: return launch_solve<0, 3, 0, 0>(a, grid, smem, st);
+    case 4: return launch_solve<0, 4, 0, 0>(a, grid, smem, st);
+    case 5: return launch_solve<0, 5, 0, 0>(a, grid, smem, st);
+    case 6: return launch_solve<0, 6, 0, 0>(a, grid, smem, st);
+    case 7: return launch_solve<0, 7, 0, 0>(a, grid, smem, st);
+    case 8: return launch_solve<1, 0, 0, 0>(a, grid, smem, st);
+    case 9: return launch_solve<1, 1, 0, 0>(a, grid, smem, st);
+    case 10: return launch_solve<1, 2, 0, 0>(a, grid, smem, st);
+    case 11: return launch_solve<1, 3, 0, 0>(a, grid, smem, st);
+    case 12: return launch_solve<1, 4, 0, 0>(a, grid, smem, st);
+    case 13: return launch_solve<1, 5, 0, 0>(a, grid, smem, st);
+    case 14: return launch_solve<1, 6, 0, 0>(a, grid, smem, st);
+    case 15: return launch_solve<1, 7, 0, 0>(a, grid, smem, st);
+    default: return launch_solve<2, 0, 0, 0>(a, grid, smem, st);
   }
 }
-
-static int solve_stride(int lam, int m) { return ((lam * m + 7) / 16) * 16 + 8; }
-
-static size_t solve_smem_bytes(int lam, int m, int P) {
-  const int S = solve_stride(lam, m);
-  size_t per_stage = (size_t)P * (BWD_SLAB > FWD_SLAB ? BWD_SLAB : FWD_SLAB) + 16 * (size_t)S;
-  return sizeof(double) * (SOLVE_STAGES * per_stage + 64 * (size_t)S);
-}
-
-template <int NT, int REM>
-static int launch_solve(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto kf = eval_solve_kernel<NT, REM, false>;
-  auto kb = eval_solve_kernel<NT, REM, true>;
-  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kf<<<grid, 256, smem, st>>>(a);
-  RP_LAUNCH_CHECK("eval_solve fwd");
-  kb<<<grid, 256, smem, st>>>(a);
-  RP_LAUNCH_CHECK("eval_solve bwd");
-  return RP_OK;
-}
-
-}  // namespace rp
-
-using namespace rp;
 
 extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m,
                              const double* tvals, int q, double* W, int64_t ldw, int* flags, void* stream) {
@@ -283,24 +42,32 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Largest chunk that fits, then the chunk minimizing (waves x chunk) over the SMs.
-  int lam_max = 0;
-  for (int lam = SOLVE_LC; lam >= 1; --lam) {
-    if ((m & 1) && (lam & 1) && q > 1) continue;  // odd m: even chunks keep chunk starts 16-byte aligned
-    if (lam * m > 256) continue;                      // one thread per (lambda, output) in the diag
-    if (solve_smem_bytes(lam, m, P) <= (size_t)maxsmem) { lam_max = lam; break; }
-  }
-  RP_REQUIRE(lam_max >= 1, "rp_eval_solve: no chunk size fits shared memory");
-  int best_lam = lam_max;
+  // Candidate chunk sizes: specialised kernels (full chunks, compile-time P) and the generic
+  // kernel; pick the lowest (waves x chunk) cost, weighting the generic kernel's overhead.
+  int best_lam = 0;
+  bool best_fast = false;
   double best_cost = 1e300;
-  for (int lam = lam_max; lam >= 1; --lam) {
-    if ((m & 1) && (lam & 1) && q > 1) continue;
+  for (int lam = SOLVE_LC; lam >= 1; --lam) {
+    if (lam * m > 256) continue;  // one thread per (lambda, output) column in the diagonal solve
+    if (solve_smem_bytes(lam, m, P) > (size_t)maxsmem) continue;
     const int chunks = (q + lam - 1) / lam;
     const long long ctas = (long long)nf * chunks;
     const double waves = (double)((ctas + sms - 1) / sms);
-    const double cost = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));  // mild preference for big chunks
-    if (cost < best_cost - 1e-9) { best_cost = cost; best_lam = lam; }
+    const double base = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));
+    const bool fast_ok = q >= lam && has_solve_fast(m, P, lam) && ((m % 2 == 0) || ((q - lam) % 2 == 0));
+    const bool gen_ok = !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks keep 16-byte alignment
+    if (fast_ok && base < best_cost - 1e-9) {
+      best_cost = base;
+      best_lam = lam;
+      best_fast = true;
+    }
+    if (gen_ok && 2.5 * base < best_cost - 1e-9) {
+      best_cost = 2.5 * base;
+      best_lam = lam;
+      best_fast = false;
+    }
   }
+  RP_REQUIRE(best_lam >= 1, "rp_eval_solve: no chunk size fits shared memory");
   SolveArgs a;
   a.theta = theta;
   a.theta_fold_stride = rp_tile_count(d) * P * 4096;
@@ -323,22 +90,6 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   const int grid = nf * a.chunks;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
   if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");
-  switch (m) {
-    case 1: return launch_solve<0, 1>(a, grid, smem, st);
-    case 2: return launch_solve<0, 2>(a, grid, smem, st);
-    case 3: return launch_solve<0, 3>(a, grid, smem, st);
-    case 4: return launch_solve<0, 4>(a, grid, smem, st);
-    case 5: return launch_solve<0, 5>(a, grid, smem, st);
-    case 6: return launch_solve<0, 6>(a, grid, smem, st);
-    case 7: return launch_solve<0, 7>(a, grid, smem, st);
-    case 8: return launch_solve<1, 0>(a, grid, smem, st);
-    case 9: return launch_solve<1, 1>(a, grid, smem, st);
-    case 10: return launch_solve<1, 2>(a, grid, smem, st);
-    case 11: return launch_solve<1, 3>(a, grid, smem, st);
-    case 12: return launch_solve<1, 4>(a, grid, smem, st);
-    case 13: return launch_solve<1, 5>(a, grid, smem, st);
-    case 14: return launch_solve<1, 6>(a, grid, smem, st);
-    case 15: return launch_solve<1, 7>(a, grid, smem, st);
-    default: return launch_solve<2, 0>(a, grid, smem, st);
-  }
+  if (best_fast) return launch_solve_fast(m, P, best_lam, a, grid, smem, st);
+  return launch_generic(m, a, grid, smem, st);
 }

@@ -194,6 +194,80 @@ def prepare_design(p, folds):
     return np.ascontiguousarray(X), np.ascontiguousarray(Y), counts
 
 
+class CvSession:
+    """A reusable device-resident piCholesky CV sweep for fixed shapes and grid.
+
+    The public entry point behind ``grid_search_pichol`` and the end-to-end bench:
+    ``run(X, Y)`` takes host arrays (numpy, or pinned torch tensors for an async
+    copy), moves them to the device, runs the sweep and returns the curves.
+    block_rows are the rows per fold block with X/Y grouped by fold.
+    With a ``dist.Shard`` the session computes its local folds and exchanges
+    Gram blocks and curves over torch.distributed.
+    """
+
+    def __init__(self, block_rows, d, m, grid_values, g=4, r=2, metric=RMSE, holdout="auto",
+                 raw_monomials=False, shard=None):
+        import torch
+
+        from . import dist
+
+        grid_values = np.asarray(grid_values, dtype=float)
+        q = grid_values.shape[0]
+        if g > q:
+            raise UsageError(f"cannot draw g={g} samples from a grid of {q}")
+        self.grid = grid_values
+        self.sample_lams = grid_values[pichol.sample_indices(q, g)]
+        self.lams, self.V, self.cond_V, self.t_scale, self.t_shift, self.P = _fit_basis_checked(
+            self.sample_lams, r, raw_monomials)
+        self.shard = shard
+        kw = {}
+        if shard is not None:
+            kw = dict(local_folds=shard.local_folds, gram_blocks=shard.gram_blocks)
+        self.engine = PicholEngine(block_rows, d, m, q, self.lams.shape[0], r, metric=metric, holdout=holdout, **kw)
+        eng = self.engine
+        self.X = torch.empty((eng.n, d), dtype=torch.float64, device=eng.device)
+        self.Y = torch.empty((eng.n, m), dtype=torch.float64, device=eng.device)
+        self.tvals = _dev.to_dev(self.t_scale * grid_values + self.t_shift)
+        self._exchange = None
+        self._gather = None
+        if shard is not None and shard.world > 1:
+            self._exchange = lambda e: dist.exchange_grams(shard, e.G, e.C, e.yy)
+            self._gather = lambda c: dist.gather_curves(shard, c)
+
+    @property
+    def h2d_bytes(self):
+        return (self.X.numel() + self.Y.numel()) * 8
+
+    @property
+    def d2h_bytes(self):
+        e = self.engine
+        return e.k * e.q * e.m * 8 + e.m * 4 + e.info.numel() * 4 + e.flags.numel() * 4
+
+    def upload(self, X, Y):
+        import torch
+
+        for dst, src in ((self.X, X), (self.Y, Y)):
+            if isinstance(src, torch.Tensor):
+                dst.copy_(src.reshape(dst.shape), non_blocking=True)
+            else:
+                dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64).reshape(dst.shape)))
+
+    def sweep(self, timings=None):
+        """Device-only sweep on the resident X/Y; returns device (curves, mean, best)."""
+        return self.engine.sweep(self.X, self.Y, self.lams, self.P, self.V, self.tvals,
+                                 exchange_grams=self._exchange, gather_curves=self._gather, timings=timings)
+
+    def run(self, X, Y, timings=None):
+        """Host in, host out: (curves (k, q, m), best index (m,)) as numpy."""
+        self.upload(X, Y)
+        curves, _, best = self.sweep(timings)
+        bad = self.engine.check_numerics(self.lams)
+        if bad is not None:
+            f, j = bad
+            raise SingularInterpolant(f"interpolated factor is singular at lambda={self.grid[j]} (fold {f})")
+        return curves.cpu().numpy(), best.cpu().numpy()
+
+
 def grid_search_pichol(
     p,
     grid,
@@ -219,25 +293,16 @@ def grid_search_pichol(
         raise UsageError(f"unknown metric {metric!r}")
     threads = resolve_threads(threads)
     t_start = time.perf_counter()
-    sample_lams = grid.values[pichol.sample_indices(grid.q, g)]
-    lams, V, cond_raw, t_scale, t_shift, Pm = _fit_basis_checked(sample_lams, r, raw_monomials)
-    X, Y, counts = prepare_design(p, folds)
-    n, d = X.shape
     if layout_kind not in trivec.ALL_KINDS:
         raise DimensionMismatch(f"unknown layout kind {layout_kind!r}")
     if layout_kind == trivec.RECURSIVE and h0 < 1:
         raise InvalidThreshold(f"recursion threshold must be >= 1, got {h0}")
-    m = Y.shape[1]
-    eng = PicholEngine(counts, d, m, grid.q, lams.shape[0], r, metric=metric, holdout=holdout)
-    dX, dY = _dev.to_dev(X), _dev.to_dev(Y)
-    tvals = t_scale * np.asarray(grid.values, dtype=float) + t_shift
+    X, Y, counts = prepare_design(p, folds)
+    n, d = X.shape
+    sess = CvSession(counts, d, Y.shape[1], grid.values, g=g, r=r, metric=metric, holdout=holdout,
+                     raw_monomials=raw_monomials)
     timings = {}
-    curves_dev, _, _ = eng.sweep(dX, dY, lams, Pm, V, tvals, timings=timings)
-    bad = eng.check_numerics(lams)
-    if bad is not None:
-        f, j = bad
-        raise SingularInterpolant(f"interpolated factor is singular at lambda={grid.values[j]} (fold {f})")
-    curves = curves_dev.cpu().numpy()
+    curves, _ = sess.run(X, Y, timings=timings)
     k = folds.k
     per_fold = _zero_timings()
     per_fold["factorize"] = timings.get("factorize", 0.0) / k
