@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -31,6 +32,12 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
+// RP_GEMM_WS=0 selects the cp.async GEMM everywhere (A/B testing of the two GEMM pipelines).
+static const bool g_use_ws = [] {
+  const char* e = getenv("RP_GEMM_WS");
+  return !(e && e[0] == '0');
+}();
+
 // ------------------------------------------------------------------ GEMM dispatch
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
@@ -42,7 +49,14 @@ static int gemm(const GemmArgs& a, int batch, cudaStream_t st, const char* name)
   if (a.lower_only && (BM != BN || a.M != a.N)) return set_error(RP_EINVAL, "%s: lower_only needs square", name);
   dim3 grid(a.lower_only ? mt * (mt + 1) / 2 : mt * nt, batch);
   size_t smem = GemmSmem<AL, BM, BN>::BYTES;
-  if (vec2) {
+  // bulk-copy (warp-specialised) path: every copied tile row must be 16-byte aligned and sized
+  const bool ws = vec2 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0) && g_use_ws;
+  if (ws) {
+    auto k = dgemm_ws_kernel<AL, BM, BN, WM, WN, EPI>;
+    size_t wsm = WsSmem<AL, BM, BN>::BYTES;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    k<<<grid, 288, wsm, st>>>(a);
+  } else if (vec2) {
     auto k = dgemm_kernel<AL, BM, BN, WM, WN, EPI, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<grid, 256, smem, st>>>(a);
