@@ -168,6 +168,11 @@ __global__ void col_sumsq_kernel(const double* Y, int64_t ldy, int64_t rows, int
 // ------------------------------------------------------------------ Cholesky
 
 constexpr int CHOL_NB = 128;
+static int CHOL_OB = [] {
+  const char* e = getenv("RP_CHOL_OB");
+  int v = e ? atoi(e) : 512;
+  return v >= 128 && v % 128 == 0 ? v : 512;
+}();
 
 // Factor the NB x NB diagonal block at (k0, k0) of every batch matrix in shared memory
 // (unblocked right-looking, LAPACK dpotf2 order: sqrt pivot, scale by reciprocal, rank-1 update),
@@ -537,43 +542,72 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   if (e != cudaSuccess) return cuda_status(e, "potrf memset");
   const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int k0 = 0; k0 < d; k0 += CHOL_NB) {
-    const int nbv = d - k0 < CHOL_NB ? d - k0 : CHOL_NB;
-    potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k0, inv, info);
-    RP_LAUNCH_CHECK("potrf_diag");
-    const int rem = d - k0 - nbv;
+  // Two-level blocked right-looking factorization. Outer panels of CHOL_OB columns are factored
+  // left-looking in 128-column blocks (update from the panel's earlier blocks as one DMMA GEMM,
+  // shared-memory diagonal factor + inverse, panel TRSM as a DMMA GEMM against the inverse);
+  // the trailing matrix then gets one SYRK with K = CHOL_OB (lower tiles only).
+  for (int k0 = 0; k0 < d; k0 += CHOL_OB) {
+    const int ob = d - k0 < CHOL_OB ? d - k0 : CHOL_OB;
+    for (int k1 = k0; k1 < k0 + ob; k1 += CHOL_NB) {
+      const int nb = k0 + ob - k1 < CHOL_NB ? k0 + ob - k1 : CHOL_NB;
+      if (k1 > k0) {
+        // A[k1:d, k1:k1+nb] -= L[k1:d, k0:k1] * L[k1:k1+nb, k0:k1]^T
+        GemmArgs u = gemm_args();
+        u.M = d - k1;
+        u.N = nb;
+        u.K = k1 - k0;
+        u.A = A + (int64_t)k0 * d + k1;
+        u.B = A + (int64_t)k0 * d + k1;
+        u.lda = u.ldb = d;
+        u.strideA = u.strideB = stride;
+        u.C = A + (int64_t)k1 * d + k1;
+        u.ldc = d;
+        u.strideC = stride;
+        u.alpha = -1.0;
+        u.beta = 1.0;
+        int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf panel update");
+        if (rc) return rc;
+      }
+      potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
+      RP_LAUNCH_CHECK("potrf_diag");
+      const int rows = d - k1 - nb;
+      if (rows > 0) {
+        // L[k1+nb:d, k1:k1+nb] = A[...] * inv(L11)^T   (in place: each CTA owns whole rows, BN >= nb)
+        double* L21 = A + (int64_t)k1 * d + k1 + nb;
+        GemmArgs t = gemm_args();
+        t.M = rows;
+        t.N = nb;
+        t.K = nb;
+        t.A = L21;
+        t.lda = d;
+        t.strideA = stride;
+        t.B = inv;
+        t.ldb = CHOL_NB;
+        t.strideB = CHOL_NB * CHOL_NB;
+        t.C = L21;
+        t.ldc = d;
+        t.strideC = stride;
+        int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(t, batch, st, "potrf trsm");
+        if (rc) return rc;
+      }
+    }
+    const int rem = d - k0 - ob;
     if (rem <= 0) break;
-    double* L21 = A + (int64_t)k0 * d + k0 + nbv;
-    // L21 = A21 * inv(L11)^T   (in place: each CTA owns whole rows since BN >= NB)
-    GemmArgs t = gemm_args();
-    t.M = rem;
-    t.N = nbv;
-    t.K = nbv;
-    t.A = L21;
-    t.lda = d;
-    t.strideA = stride;
-    t.B = inv;
-    t.ldb = CHOL_NB;
-    t.strideB = CHOL_NB * CHOL_NB;
-    t.C = L21;
-    t.ldc = d;
-    t.strideC = stride;
-    int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(t, batch, st, "potrf trsm");
-    if (rc) return rc;
-    // A22 -= L21 L21^T (lower tiles)
+    // A22 -= L21 L21^T with K = ob (lower tiles)
+    const double* L21 = A + (int64_t)k0 * d + k0 + ob;
     GemmArgs u = gemm_args();
     u.M = u.N = rem;
-    u.K = nbv;
+    u.K = ob;
     u.A = u.B = L21;
     u.lda = u.ldb = d;
     u.strideA = u.strideB = stride;
-    u.C = A + (int64_t)(k0 + nbv) * d + k0 + nbv;
+    u.C = A + (int64_t)(k0 + ob) * d + k0 + ob;
     u.ldc = d;
     u.strideC = stride;
     u.alpha = -1.0;
     u.beta = 1.0;
     u.lower_only = 1;
-    rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf syrk");
+    int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf syrk");
     if (rc) return rc;
   }
   return RP_OK;

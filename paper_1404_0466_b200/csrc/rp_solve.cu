@@ -55,7 +55,7 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
     const double waves = (double)((ctas + sms - 1) / sms);
     const double base = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));
     const bool fast_ok = q >= lam && has_solve_fast(m, P, lam) && ((m % 2 == 0) || ((q - lam) % 2 == 0));
-    const bool gen_ok = !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks keep 16-byte alignment
+    const bool gen_ok = lam <= SOLVE_LC_GENERIC && !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks
     if (fast_ok && base < best_cost - 1e-9) {
       best_cost = base;
       best_lam = lam;

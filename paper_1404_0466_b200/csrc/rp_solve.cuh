@@ -25,7 +25,8 @@
 
 namespace rp {
 
-constexpr int SOLVE_LC = 16;     // max lambdas per CTA
+constexpr int SOLVE_LC = 16;          // max lambdas per CTA (specialised kernels)
+constexpr int SOLVE_LC_GENERIC = 8;   // max lambdas per CTA (generic kernel)
 constexpr int SOLVE_PMAX = 5;    // max polynomial planes (degree <= 4)
 constexpr int SOLVE_STAGES = 3;
 constexpr int FWD_SLAB = 16 * 68;   // per plane: 16 columns x 64 rows (stride 68)
@@ -50,11 +51,18 @@ RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 // With LCT > 0 every chunk is full: the last chunk starts at q - LCT and recomputes a few
 // lambdas of its neighbour; per-lambda arithmetic is independent of the chunk, so the
 // duplicated writes are bit-identical.
+//
+// Warp layout: 8 warps = 4 row groups (16 rows = 2 DMMA m-tiles each) x 2 lambda groups, so
+// every W fragment loaded from shared memory feeds two DMMAs and every coefficient fragment
+// is evaluated for half of the chunk's lambdas.
 template <int NT, int REM, int PT, int LCT, bool BWD>
 __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
-  constexpr int LC = LCT ? LCT : SOLVE_LC;
+  constexpr int LC = LCT ? LCT : SOLVE_LC_GENERIC;
+  constexpr int LH = (LC + 1) / 2;
   constexpr int PM = PT ? PT : SOLVE_PMAX;
   constexpr int REMA = REM > 0 ? REM : 1;
+  constexpr int NTA = NT > 0 ? NT : 1;
+  constexpr bool REM2 = (REM % 2) == 0;
   constexpr int SLAB = BWD ? BWD_SLAB : FWD_SLAB;
   extern __shared__ __align__(16) double smem[];
   const int P = PT ? PT : a.P;
@@ -68,33 +76,39 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
+  const int rg = warp & 3, lg = warp >> 2;
   const int fold = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
   const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
   const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
   if (nl <= 0) return;
   const double* theta = a.theta + fold * a.theta_fold_stride;
   double* W = a.W + fold * a.w_fold_stride;
-  const int cw = nl * m;            // valid chunk columns
+  const int cw = nl * m;             // valid chunk columns
   const int cpairs = (cw + 1) >> 1;  // 16-byte copies per W row
   const int64_t wcol0 = (int64_t)l0 * m;
 
-  double tl[LC];
+  double tl[LH];
 #pragma unroll
-  for (int l = 0; l < LC; ++l) tl[l] = (l < nl) ? a.tvals[l0 + l] : 0.0;
+  for (int i = 0; i < LH; ++i) {
+    const int l = lg * LH + i;
+    tl[i] = (l < nl) ? a.tvals[l0 + l] : 0.0;
+  }
 
-  double acc[LC][NT > 0 ? NT : 1][2];
-  double accx[LC][REMA];
+  double acc[LH][2][NTA][2];
+  double accx[LH][2][REMA];
 
   for (int step = 0; step < a.nt; ++step) {
     const int I = BWD ? (a.nt - 1 - step) : step;
     const int nslab = 4 * (BWD ? (a.nt - 1 - I) : I);
 #pragma unroll
-    for (int l = 0; l < LC; ++l) {
+    for (int i = 0; i < LH; ++i)
 #pragma unroll
-      for (int j = 0; j < (NT > 0 ? NT : 1); ++j) acc[l][j][0] = acc[l][j][1] = 0.0;
+      for (int mt = 0; mt < 2; ++mt) {
 #pragma unroll
-      for (int c = 0; c < REMA; ++c) accx[l][c] = 0.0;
-    }
+        for (int j = 0; j < NTA; ++j) acc[i][mt][j][0] = acc[i][mt][j][1] = 0.0;
+#pragma unroll
+        for (int c = 0; c < REMA; ++c) accx[i][mt][c] = 0.0;
+      }
 
     auto issue = [&](int s) {
       if (s < nslab) {
@@ -134,28 +148,46 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const int k = ks * 4 + t;
-        double th[PM];
+        double th[2][PM];
 #pragma unroll
-        for (int p = 0; p < PM; ++p) {
-          if (p < P) th[p] = BWD ? T[p * BWD_SLAB + (warp * 8 + g) * 20 + k] : T[p * FWD_SLAB + k * 68 + warp * 8 + g];
+        for (int mt = 0; mt < 2; ++mt) {
+          const int row = rg * 16 + mt * 8 + g;
+#pragma unroll
+          for (int p = 0; p < PM; ++p)
+            if (p < P) th[mt][p] = BWD ? T[p * BWD_SLAB + row * 20 + k] : T[p * FWD_SLAB + k * 68 + row];
         }
         const double* wrow = Wb + k * S;
 #pragma unroll
-        for (int l = 0; l < LC; ++l) {
+        for (int i = 0; i < LH; ++i) {
+          const int l = lg * LH + i;
           if (l < nl) {
-            // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
-            double av = 0.0;
+            double b[NTA];
 #pragma unroll
-            for (int p = PM - 1; p >= 0; --p) {
-              if (p < P) av = (p == P - 1) ? th[p] : fma(av, tl[l], th[p]);
+            for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
+            double rv[REMA];
+            if (REM2) {
+#pragma unroll
+              for (int c = 0; c < REM; c += 2) {
+                const double2 v2 = *reinterpret_cast<const double2*>(wrow + l * m + NT * 8 + c);
+                rv[c] = v2.x;
+                rv[c + 1] = v2.y;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
             }
 #pragma unroll
-            for (int j = 0; j < NT; ++j) {
-              double b = wrow[l * m + j * 8 + g];
-              dmma884(acc[l][j][0], acc[l][j][1], av, b);
-            }
+            for (int mt = 0; mt < 2; ++mt) {
+              // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
+              double av = 0.0;
 #pragma unroll
-            for (int c = 0; c < REM; ++c) accx[l][c] = fma(av, wrow[l * m + NT * 8 + c], accx[l][c]);
+              for (int p = PM - 1; p >= 0; --p)
+                if (p < P) av = (p == P - 1) ? th[mt][p] : fma(av, tl[i], th[mt][p]);
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
+#pragma unroll
+              for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+            }
           }
         }
       }
@@ -174,38 +206,41 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
     }
     const int rowI = I * 64;
 #pragma unroll
-    for (int l = 0; l < LC; ++l) {
+    for (int i = 0; i < LH; ++i) {
+      const int l = lg * LH + i;
       if (l < nl) {
 #pragma unroll
-        for (int c = 0; c < REM; ++c) {
-          double v = accx[l][c];
-          v += __shfl_xor_sync(0xffffffffu, v, 1);
-          v += __shfl_xor_sync(0xffffffffu, v, 2);
-          accx[l][c] = v;
-        }
-        const int i = warp * 8 + g;
-#pragma unroll
-        for (int j = 0; j < NT; ++j) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int col = j * 8 + 2 * t + h;
-            double base = BWD ? W[(int64_t)(rowI + i) * a.ldw + wcol0 + l * m + col]
-                              : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + i) * m + col];
-            sR[i * S + l * m + col] = base - acc[l][j][h];
-          }
-        }
-        if (t == 0) {
+        for (int mt = 0; mt < 2; ++mt) {
+          const int row = rg * 16 + mt * 8 + g;
 #pragma unroll
           for (int c = 0; c < REM; ++c) {
-            const int col = NT * 8 + c;
-            double base = BWD ? W[(int64_t)(rowI + i) * a.ldw + wcol0 + l * m + col]
-                              : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + i) * m + col];
-            sR[i * S + l * m + col] = base - accx[l][c];
+            double v = accx[i][mt][c];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            accx[i][mt][c] = v;
+          }
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = j * 8 + 2 * t + h;
+              double base = BWD ? W[(int64_t)(rowI + row) * a.ldw + wcol0 + l * m + col]
+                                : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + row) * m + col];
+              sR[row * S + l * m + col] = base - acc[i][mt][j][h];
+            }
+          }
+          if (t == 0) {
+#pragma unroll
+            for (int c = 0; c < REM; ++c) {
+              const int col = NT * 8 + c;
+              double base = BWD ? W[(int64_t)(rowI + row) * a.ldw + wcol0 + l * m + col]
+                                : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + row) * m + col];
+              sR[row * S + l * m + col] = base - accx[i][mt][c];
+            }
           }
         }
       }
     }
-    __syncthreads();
     cp_async_wait<0>();
     __syncthreads();
     if (tid < cw) {
