@@ -55,10 +55,11 @@ RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 // Warp layout: 8 warps = 4 row groups (16 rows = 2 DMMA m-tiles each) x 2 lambda groups, so
 // every W fragment loaded from shared memory feeds two DMMAs and every coefficient fragment
 // is evaluated for half of the chunk's lambdas.
-template <int NT, int REM, int PT, int LCT, bool BWD>
-__global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
+template <int NT, int REM, int PT, int LCT, int LG, bool BWD>
+__global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
+  constexpr int NTH = 128 * LG;  // 4 row groups x LG lambda groups of warps
   constexpr int LC = LCT ? LCT : SOLVE_LC_GENERIC;
-  constexpr int LH = (LC + 1) / 2;
+  constexpr int LH = (LC + LG - 1) / LG;
   constexpr int PM = PT ? PT : SOLVE_PMAX;
   constexpr int REMA = REM > 0 ? REM : 1;
   constexpr int NTA = NT > 0 ? NT : 1;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int rg = warp & 3, lg = warp >> 2;
+  const int rg = warp & 3, lg = warp >> 2;  // row group, lambda group
   const int fold = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
   const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
   const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
         const int kq = s & 3;
         const double* tile = theta + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * 4096;
         double* dT = sT + st * stageT;
-        for (int c = tid; c < P * 512; c += 256) {
+        for (int c = tid; c < P * 512; c += NTH) {
           const int p = c >> 9, e = c & 511;
           if (!BWD) {
             const int kk = e >> 5, i2 = (e & 31) * 2;  // column kq*16+kk, rows i2, i2+1
@@ -129,10 +130,9 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
         }
         double* dW = sW + st * stageW;
         const double* src = W + (int64_t)(J * 64 + kq * 16) * a.ldw + wcol0;
-        for (int c = tid; c < 16 * cpairs; c += 256) {
-          const int kk = c / cpairs, c2 = (c - kk * cpairs) * 2;
-          cp_async16(dW + kk * S + c2, src + (int64_t)kk * a.ldw + c2, true);
-        }
+        for (int kk = warp; kk < 16; kk += NTH / 32)
+          for (int c2 = 2 * lane; c2 < 2 * cpairs; c2 += 64)
+            cp_async16(dW + kk * S + c2, src + (int64_t)kk * a.ldw + c2, true);
       }
       cp_async_commit();
     };
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
     double* sD = smem;  // union with the ring (idle during the diagonal step)
     {
       const double* tile = theta + (int64_t)tile_index(I, I) * P * 4096;
-      for (int c = tid; c < P * 2048; c += 256) cp_async16(sD + 2 * c, tile + 2 * c, true);
+      for (int c = tid; c < P * 2048; c += NTH) cp_async16(sD + 2 * c, tile + 2 * c, true);
       cp_async_commit();
     }
     const int rowI = I * 64;
@@ -293,9 +293,9 @@ __global__ void __launch_bounds__(256, 1) eval_solve_kernel(SolveArgs a) {
       }
     }
     __syncthreads();
-    for (int e = tid; e < 64 * cw; e += 256) {
-      const int i = e / cw, c = e - (e / cw) * cw;
-      W[(int64_t)(rowI + i) * a.ldw + wcol0 + c] = sR[i * S + c];
+    for (int i = warp; i < 64; i += NTH / 32) {
+      double* dst = W + (int64_t)(rowI + i) * a.ldw + wcol0;
+      for (int c = lane; c < cw; c += 32) dst[c] = sR[i * S + c];
     }
     __syncthreads();
   }
@@ -312,15 +312,15 @@ inline size_t solve_smem_bytes(int lam, int m, int P) {
 }
 
 
-template <int NT, int REM, int PT, int LCT>
+template <int NT, int REM, int PT, int LCT, int LG = 2>
 int launch_solve(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto kf = eval_solve_kernel<NT, REM, PT, LCT, false>;
-  auto kb = eval_solve_kernel<NT, REM, PT, LCT, true>;
+  auto kf = eval_solve_kernel<NT, REM, PT, LCT, LG, false>;
+  auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, true>;
   cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kf<<<grid, 256, smem, st>>>(a);
+  kf<<<grid, 128 * LG, smem, st>>>(a);
   RP_LAUNCH_CHECK("eval_solve fwd");
-  kb<<<grid, 256, smem, st>>>(a);
+  kb<<<grid, 128 * LG, smem, st>>>(a);
   RP_LAUNCH_CHECK("eval_solve bwd");
   return RP_OK;
 }

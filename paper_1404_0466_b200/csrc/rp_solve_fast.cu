@@ -3,6 +3,10 @@
 // m = 1 (c1), m = 10 (c2-c4, degree 2), m = 16 (c5, degree 3).
 #include "rp_solve.cuh"
 
+#ifndef RP_SOLVE_LG
+#define RP_SOLVE_LG 4
+#endif
+
 namespace rp {
 
 #define RP_FAST_LIST(X) \
@@ -18,7 +22,7 @@ bool has_solve_fast(int m, int P, int lam) {
 
 int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
 #define RP_LAUNCH(M, PP, L) \
-  if (m == M && P == PP && lam == L) return launch_solve<(M) / 8, (M) % 8, PP, L>(a, grid, smem, st);
+  if (m == M && P == PP && lam == L) return launch_solve<(M) / 8, (M) % 8, PP, L, RP_SOLVE_LG>(a, grid, smem, st);
   RP_FAST_LIST(RP_LAUNCH)
 #undef RP_LAUNCH
   return -2;
