@@ -11,6 +11,7 @@
 
 #include "rp_common.cuh"
 #include "rp_gemm.cuh"
+#include "rp_potrf_diag.cuh"
 #include "../../include/ridgepath_b200.h"
 
 namespace rp {
@@ -31,6 +32,12 @@ static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// RP_POTRF_DIAG=simple selects the unblocked shared-memory diagonal factor (A/B testing).
+static const bool g_simple_diag = [] {
+  const char* e = getenv("RP_POTRF_DIAG");
+  return e && e[0] == 's';
+}();
 
 // RP_GEMM_WS=0 selects the cp.async GEMM everywhere (A/B testing of the two GEMM pipelines).
 static const bool g_use_ws = [] {
@@ -542,6 +549,7 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   if (e != cudaSuccess) return cuda_status(e, "potrf memset");
   const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(potrf_diag_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PD_SMEM);
   // Two-level blocked right-looking factorization. Outer panels of CHOL_OB columns are factored
   // left-looking in 128-column blocks (update from the panel's earlier blocks as one DMMA GEMM,
   // shared-memory diagonal factor + inverse, panel TRSM as a DMMA GEMM against the inverse);
@@ -568,7 +576,11 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
         int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf panel update");
         if (rc) return rc;
       }
-      potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
+      if (g_simple_diag) {
+        potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
+      } else {
+        potrf_diag_dmma_kernel<<<batch, PD_THREADS, PD_SMEM, st>>>(A, d, stride, k1, inv, info);
+      }
       RP_LAUNCH_CHECK("potrf_diag");
       const int rows = d - k1 - nb;
       if (rows > 0) {
