@@ -62,7 +62,12 @@ static int gemm(const GemmArgs& a, int batch, cudaStream_t st, const char* name)
     auto k = dgemm_ws_kernel<AL, BM, BN, WM, WN, EPI>;
     size_t wsm = WsSmem<AL, BM, BN>::BYTES;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
-    k<<<grid, 288, wsm, st>>>(a);
+    const int total = (int)grid.x * batch;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ctas = total < sms ? total : sms;  // persistent: one CTA per SM walks the tile list
+    k<<<ctas, 288, wsm, st>>>(a, total);
   } else if (vec2) {
     auto k = dgemm_kernel<AL, BM, BN, WM, WN, EPI, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -126,16 +131,19 @@ __global__ void gram_sum_kernel(const double* G, int nblocks, int d, double* Gsu
   Gsum[e] = s;
 }
 
+// One pass per fold: H_f = Gsum - G_f read once, all s shifted copies written (lower triangle,
+// column by column so the threads of a block stay on contiguous rows).
 __global__ void fold_shift_kernel(const double* Gsum, const double* G, int d, int s, FoldSysArgs fa, double* A) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t n = (int64_t)d * d;
-  if (e >= n) return;
-  int i = (int)(e % d), j = (int)(e / d);
-  if (i < j) return;
-  const int fs = blockIdx.y, f = fs / s, si = fs % s;
-  double v = Gsum[e] - G[fa.folds[f] * n + e];
-  if (i == j) v += fa.lams[si];
-  A[fs * n + e] = v;
+  const int j = blockIdx.x;  // column
+  const int f = blockIdx.y;
+  const int64_t n = (int64_t)d * d;
+  const double* gs = Gsum + (int64_t)j * d;
+  const double* gf = G + fa.folds[f] * n + (int64_t)j * d;
+  double* out = A + (int64_t)f * s * n + (int64_t)j * d;
+  for (int i = j + threadIdx.x; i < d; i += blockDim.x) {
+    const double v = __ldcs(gs + i) - __ldcs(gf + i);
+    for (int si = 0; si < s; ++si) __stcs(out + si * n + i, (i == j) ? v + fa.lams[si] : v);
+  }
 }
 
 __global__ void fold_rhs_kernel(const double* C, int nblocks, int d, int dp, int m, FoldSysArgs fa, double* rhs) {
@@ -525,7 +533,7 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
   gram_sum_kernel<<<grid1d(n), 256, 0, st>>>(G, nblocks, d, Gsum);
   RP_LAUNCH_CHECK("gram_sum");
   if (A) {
-    fold_shift_kernel<<<dim3(grid1d(n), nf * s), 256, 0, st>>>(Gsum, G, d, s, fa, A);
+    fold_shift_kernel<<<dim3(d, nf), 256, 0, st>>>(Gsum, G, d, s, fa, A);
     RP_LAUNCH_CHECK("fold_shift");
   }
   if (rhs && m > 0) {

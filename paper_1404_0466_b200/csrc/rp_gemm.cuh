@@ -255,22 +255,47 @@ __global__ void __launch_bounds__(256) dgemm_kernel(GemmArgs p) {
 
 
 // ---------------------------------------------------------------------------------------------
-// Warp-specialised variant (the default on aligned operands): warp 8 is a producer that moves
-// each k-tile with 1-D bulk async copies (cp.async.bulk, one per contiguous tile row) into the
-// padded shared-memory rows and signals a full-mbarrier with the transaction byte count; warps
-// 0-7 only issue LDS + DMMA and release the stage through an empty-mbarrier. No block-wide
-// barrier in the main loop, so warps drift and the DMMA pipe stays fed across stage boundaries.
+// Warp-specialised persistent variant (the default on aligned operands). One CTA per SM walks
+// the (batch, tile) list; warp 8 is a producer that moves each 16-deep k-tile with 1-D bulk async
+// copies (cp.async.bulk, one per contiguous tile row) into padded shared-memory rows and signals
+// a full-mbarrier with the transaction byte count; warps 0-7 only issue LDS + DMMA and release
+// the stage through an empty-mbarrier. The stage ring runs continuously across tiles, so the
+// producer prefetches the next tile while the consumers run the previous tile's epilogue; there
+// is no block-wide barrier in the main loop.
 constexpr int WS_STAGES = 4;
 
 template <int AL, int BM, int BN>
 struct WsSmem {
   using B = GemmSmem<AL, BM, BN>;
   static constexpr size_t DATA = sizeof(double) * WS_STAGES * (B::A_ELEMS + B::B_ELEMS);
-  static constexpr size_t BYTES = DATA + 2 * WS_STAGES * sizeof(uint64_t);
+  static constexpr size_t RED = sizeof(double) * 8 * BN;  // reduction epilogue scratch (<= 8 row groups)
+  static constexpr size_t BYTES = DATA + RED + 2 * WS_STAGES * sizeof(uint64_t);
 };
 
+struct TileCoord {
+  int batch, tm, tn;
+};
+
+RP_DEVINL TileCoord ws_tile(const GemmArgs& p, int tile, int mtiles, int ntiles) {
+  const int per = p.lower_only ? mtiles * (mtiles + 1) / 2 : mtiles * ntiles;
+  TileCoord c;
+  c.batch = tile / per;
+  int lin = tile - c.batch * per;
+  if (p.lower_only) {
+    int tm = (int)((sqrt(8.0 * lin + 1.0) - 1.0) * 0.5);
+    while ((tm + 1) * (tm + 2) / 2 <= lin) ++tm;
+    while (tm * (tm + 1) / 2 > lin) --tm;
+    c.tm = tm;
+    c.tn = lin - tm * (tm + 1) / 2;
+  } else {
+    c.tm = lin % mtiles;
+    c.tn = lin / mtiles;
+  }
+  return c;
+}
+
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
-__global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p) {
+__global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_tiles) {
   constexpr int BK = GEMM_BK;
   constexpr int MT = WM / 8, NT = WN / 8;
   constexpr int WARPS_M = BM / WM;
@@ -279,25 +304,12 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p) {
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + WS_STAGES * SM::A_ELEMS;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + WS_STAGES * (SM::A_ELEMS + SM::B_ELEMS));
+  double* red = smem + WS_STAGES * (SM::A_ELEMS + SM::B_ELEMS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 8 * BN);
   uint64_t* empty = full + WS_STAGES;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int batch = blockIdx.y;
-  const int mtiles = (p.M + BM - 1) / BM;
-  int tm, tn;
-  if (p.lower_only) {
-    int lin = blockIdx.x;
-    tm = (int)((sqrt(8.0 * lin + 1.0) - 1.0) * 0.5);
-    while ((tm + 1) * (tm + 2) / 2 <= lin) ++tm;
-    while (tm * (tm + 1) / 2 > lin) --tm;
-    tn = lin - tm * (tm + 1) / 2;
-  } else {
-    tm = blockIdx.x % mtiles;
-    tn = blockIdx.x / mtiles;
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int mv = min(BM, p.M - m0), nv = min(BN, p.N - n0);
+  const int mtiles = (p.M + BM - 1) / BM, ntiles = (p.N + BN - 1) / BN;
   const int ktiles = (p.K + BK - 1) / BK;
 
   if (tid == 0) {
@@ -311,45 +323,50 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p) {
 
   if (warp == 8) {
     // ---------------- producer ----------------
-    const double* A = p.A + batch * p.strideA;
-    const double* B = p.B + batch * p.strideB;
-    for (int kt = 0; kt < ktiles; ++kt) {
-      const int st = kt % WS_STAGES;
-      mbar_wait(&empty[st], ((kt / WS_STAGES) & 1) ^ 1);
-      const int k0 = kt * BK, kv = min(BK, p.K - k0);
-      double* dA = sA + st * SM::A_ELEMS;
-      double* dB = sB + st * SM::B_ELEMS;
-      // zero the out-of-range parts of the stage (edge tiles only)
-      if (AL == A_KMAJOR) {
-        if (kv < BK || mv < BM)
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      const TileCoord tc = ws_tile(p, tile, mtiles, ntiles);
+      const int m0 = tc.tm * BM, n0 = tc.tn * BN;
+      const int mv = min(BM, p.M - m0), nv = min(BN, p.N - n0);
+      const double* A = p.A + tc.batch * p.strideA;
+      const double* B = p.B + tc.batch * p.strideB;
+      for (int kt = 0; kt < ktiles; ++kt, ++it) {
+        const int st = it % WS_STAGES;
+        mbar_wait(&empty[st], ((it / WS_STAGES) & 1) ^ 1);
+        const int k0 = kt * BK, kv = min(BK, p.K - k0);
+        double* dA = sA + st * SM::A_ELEMS;
+        double* dB = sB + st * SM::B_ELEMS;
+        // zero the out-of-range parts of the stage (edge tiles only)
+        if (kv < BK || mv < BM) {
           for (int e = lane; e < BK * BM; e += 32) {
-            int kk = e / BM, mm = e % BM;
-            if (kk >= kv || mm >= mv) dA[kk * SM::A_STRIDE + mm] = 0.0;
+            if (AL == A_KMAJOR) {
+              const int kk = e / BM, mm = e % BM;
+              if (kk >= kv || mm >= mv) dA[kk * SM::A_STRIDE + mm] = 0.0;
+            } else {
+              const int mm = e / BK, kk = e % BK;
+              if (kk >= kv || mm >= mv) dA[mm * SM::A_STRIDE + kk] = 0.0;
+            }
           }
-      } else {
-        if (kv < BK || mv < BM)
-          for (int e = lane; e < BK * BM; e += 32) {
-            int mm = e / BK, kk = e % BK;
-            if (kk >= kv || mm >= mv) dA[mm * SM::A_STRIDE + kk] = 0.0;
-          }
-      }
-      if (kv < BK || nv < BN)
-        for (int e = lane; e < BK * BN; e += 32) {
-          int kk = e / BN, nn = e % BN;
-          if (kk >= kv || nn >= nv) dB[kk * SM::B_STRIDE + nn] = 0.0;
         }
-      __syncwarp();
-      const uint32_t bytesA = (uint32_t)(kv * mv * 8), bytesB = (uint32_t)(kv * nv * 8);
-      if (lane == 0) mbar_arrive_expect_tx(&full[st], bytesA + bytesB);
-      if (AL == A_KMAJOR) {
+        if (kv < BK || nv < BN)
+          for (int e = lane; e < BK * BN; e += 32) {
+            const int kk = e / BN, nn = e % BN;
+            if (kk >= kv || nn >= nv) dB[kk * SM::B_STRIDE + nn] = 0.0;
+          }
+        __syncwarp();
+        const uint32_t bytesA = (uint32_t)(kv * mv * 8), bytesB = (uint32_t)(kv * nv * 8);
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], bytesA + bytesB);
+        __syncwarp();
+        if (AL == A_KMAJOR) {
+          for (int kk = lane; kk < kv; kk += 32)
+            bulk_g2s(dA + kk * SM::A_STRIDE, A + (int64_t)(k0 + kk) * p.lda + m0, (uint32_t)(mv * 8), &full[st]);
+        } else {
+          for (int mm = lane; mm < mv; mm += 32)
+            bulk_g2s(dA + mm * SM::A_STRIDE, A + (int64_t)(m0 + mm) * p.lda + k0, (uint32_t)(kv * 8), &full[st]);
+        }
         for (int kk = lane; kk < kv; kk += 32)
-          bulk_g2s(dA + kk * SM::A_STRIDE, A + (int64_t)(k0 + kk) * p.lda + m0, (uint32_t)(mv * 8), &full[st]);
-      } else {
-        for (int mm = lane; mm < mv; mm += 32)
-          bulk_g2s(dA + mm * SM::A_STRIDE, A + (int64_t)(m0 + mm) * p.lda + k0, (uint32_t)(kv * 8), &full[st]);
+          bulk_g2s(dB + kk * SM::B_STRIDE, B + (int64_t)(k0 + kk) * p.ldb + n0, (uint32_t)(nv * 8), &full[st]);
       }
-      for (int kk = lane; kk < kv; kk += 32)
-        bulk_g2s(dB + kk * SM::B_STRIDE, B + (int64_t)(k0 + kk) * p.ldb + n0, (uint32_t)(nv * 8), &full[st]);
     }
     return;
   }
@@ -357,114 +374,139 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p) {
   // ---------------- consumers ----------------
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
-  double acc[MT][NT][2];
+  int it = 0;
+  for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    const TileCoord tc = ws_tile(p, tile, mtiles, ntiles);
+    const int m0 = tc.tm * BM, n0 = tc.tn * BN;
+    const int batch = tc.batch;
+    double acc[MT][NT][2];
 #pragma unroll
-  for (int i = 0; i < MT; ++i)
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int st = kt % WS_STAGES;
-    mbar_wait(&full[st], (kt / WS_STAGES) & 1);
-    const double* a_s = sA + st * SM::A_ELEMS;
-    const double* b_s = sB + st * SM::B_ELEMS;
+    for (int kt = 0; kt < ktiles; ++kt, ++it) {
+      const int st = it % WS_STAGES;
+      mbar_wait(&full[st], (it / WS_STAGES) & 1);
+      const double* a_s = sA + st * SM::A_ELEMS;
+      const double* b_s = sB + st * SM::B_ELEMS;
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int k = ks * 4 + t;
-      double af[MT], bf[NT];
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int k = ks * 4 + t;
+        double af[MT], bf[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          int row = wm * WM + i * 8 + g;
+          af[i] = (AL == A_KMAJOR) ? a_s[k * SM::A_STRIDE + row] : a_s[row * SM::A_STRIDE + k];
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) bf[j] = b_s[k * SM::B_STRIDE + wn * WN + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+
+    if (EPI == EPI_STORE) {
+      double* C = p.C + batch * p.strideC;
+      if (p.beta != 0.0) {
+        // issue every C load before any store (stores could alias later loads otherwise,
+        // which serialises 64 global round trips per thread)
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int row = m0 + wm * WM + i * 8 + g;
+#pragma unroll
+          for (int j = 0; j < NT; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = n0 + wn * WN + j * 8 + 2 * t + h;
+              const double old = (row < p.M && col < p.N) ? __ldcg(C + (int64_t)col * p.ldc + row) : 0.0;
+              acc[i][j][h] = fma(p.beta, old, p.alpha * acc[i][j][h]);
+            }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            acc[i][j][0] *= p.alpha;
+            acc[i][j][1] *= p.alpha;
+          }
+      }
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
-        int row = wm * WM + i * 8 + g;
-        af[i] = (AL == A_KMAJOR) ? a_s[k * SM::A_STRIDE + row] : a_s[row * SM::A_STRIDE + k];
-      }
+        const int row = m0 + wm * WM + i * 8 + g;
+        if (row >= p.M) continue;
 #pragma unroll
-      for (int j = 0; j < NT; ++j) bf[j] = b_s[k * SM::B_STRIDE + wn * WN + j * 8 + g];
+        for (int j = 0; j < NT; ++j) {
 #pragma unroll
-      for (int i = 0; i < MT; ++i)
-#pragma unroll
-        for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-  }
-
-  if (EPI == EPI_STORE) {
-    double* C = p.C + batch * p.strideC;
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      int row = m0 + wm * WM + i * 8 + g;
-      if (row >= p.M) continue;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int col = n0 + wn * WN + j * 8 + 2 * t + h;
-          if (col >= p.N) continue;
-          double* c = C + (int64_t)col * p.ldc + row;
-          double v = p.alpha * acc[i][j][h];
-          if (p.beta != 0.0) v = fma(p.beta, *c, v);
-          *c = v;
-        }
-      }
-    }
-  } else {
-    const double* Yb = p.Y + batch * p.strideY;
-    double colsum[NT][2];
-#pragma unroll
-    for (int j = 0; j < NT; ++j) colsum[j][0] = colsum[j][1] = 0.0;
-#pragma unroll
-    for (int i = 0; i < MT; ++i) {
-      int row = m0 + wm * WM + i * 8 + g;
-      if (row >= p.M) continue;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int col = n0 + wn * WN + j * 8 + 2 * t + h;
-          if (col >= p.N) continue;
-          double v;
-          if (EPI == EPI_SSE) {
-            double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
-            double e = acc[i][j][h] - y;
-            v = e * e;
-          } else if (EPI == EPI_MIS) {
-            double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
-            double s_pred = acc[i][j][h] >= 0.0 ? 1.0 : -1.0;
-            double s_y = (y > 0.0) ? 1.0 : ((y < 0.0) ? -1.0 : 0.0);
-            v = (s_pred != s_y) ? 1.0 : 0.0;
-          } else {
-            v = acc[i][j][h] * Yb[(int64_t)row * p.ldy + col];
+          for (int h = 0; h < 2; ++h) {
+            const int col = n0 + wn * WN + j * 8 + 2 * t + h;
+            if (col < p.N) C[(int64_t)col * p.ldc + row] = acc[i][j][h];
           }
-          colsum[j][h] += v;
         }
       }
-    }
+    } else {
+      const double* Yb = p.Y + batch * p.strideY;
+      double colsum[NT][2];
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+      for (int j = 0; j < NT; ++j) colsum[j][0] = colsum[j][1] = 0.0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        double v = colsum[j][h];
-        v += __shfl_xor_sync(0xffffffffu, v, 4);
-        v += __shfl_xor_sync(0xffffffffu, v, 8);
-        v += __shfl_xor_sync(0xffffffffu, v, 16);
-        colsum[j][h] = v;
+      for (int i = 0; i < MT; ++i) {
+        int row = m0 + wm * WM + i * 8 + g;
+        if (row >= p.M) continue;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int col = n0 + wn * WN + j * 8 + 2 * t + h;
+            if (col >= p.N) continue;
+            double v;
+            if (EPI == EPI_SSE) {
+              double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
+              double e = acc[i][j][h] - y;
+              v = e * e;
+            } else if (EPI == EPI_MIS) {
+              double y = Yb[(int64_t)row * p.ldy + (col % p.ycols)];
+              double s_pred = acc[i][j][h] >= 0.0 ? 1.0 : -1.0;
+              double s_y = (y > 0.0) ? 1.0 : ((y < 0.0) ? -1.0 : 0.0);
+              v = (s_pred != s_y) ? 1.0 : 0.0;
+            } else {
+              v = acc[i][j][h] * Yb[(int64_t)row * p.ldy + col];
+            }
+            colsum[j][h] += v;
+          }
+        }
       }
-    named_bar_sync(1, 256);
-    double* red = smem;  // [WARPS_M][BN]; all stages are drained
-    if (g == 0) {
 #pragma unroll
       for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) red[wm * BN + wn * WN + j * 8 + 2 * t + h] = colsum[j][h];
-    }
-    named_bar_sync(1, 256);
-    for (int c = tid; c < BN; c += 256) {
-      int col = n0 + c;
-      if (col >= p.N) continue;
-      double s = 0.0;
+        for (int h = 0; h < 2; ++h) {
+          double v = colsum[j][h];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          colsum[j][h] = v;
+        }
+      named_bar_sync(1, 256);  // previous tile's readers of red are done
+      if (g == 0) {
 #pragma unroll
-      for (int w = 0; w < WARPS_M; ++w) s += red[w * BN + c];
-      p.partial[((int64_t)batch * mtiles + tm) * p.N + col] = s;
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) red[wm * BN + wn * WN + j * 8 + 2 * t + h] = colsum[j][h];
+      }
+      named_bar_sync(1, 256);
+      for (int c = tid; c < BN; c += 256) {
+        int col = n0 + c;
+        if (col >= p.N) continue;
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < WARPS_M; ++w) s += red[w * BN + c];
+        p.partial[((int64_t)batch * mtiles + tc.tm) * p.N + col] = s;
+      }
     }
   }
 }
