@@ -26,11 +26,15 @@
  * Packed-factor layout ("tile" layout): the order-d
  * lower triangle is cut into 64 x 64 tiles (I, J), I >= J, d padded up to
  * dp = 64 * ceil(d / 64). Tile (I, J) is stored at tile index I(I+1)/2 + J;
- * a tile holds P = r + 1 coefficient planes, each 64 x 64 column-major
- * (element (i, j) of plane p at p*4096 + j*64 + i). Entries above the
- * diagonal of a diagonal tile are 0; padded diagonal entries are 1 in plane 0
- * (the identity) so solves stay well defined. Per fold the buffer holds
- * rp_tile_count(d) * P * 4096 doubles.
+ * a tile holds P = r + 1 coefficient planes of 64 x 64 with a padded leading
+ * dimension of 68 (TP = 64*68 doubles per plane). Each fold's buffer holds two
+ * copies: the forward copy (plane p of tile t at (t*P + p)*TP, element (i, j)
+ * at j*68 + i, column-major) followed by the transposed backward copy (same
+ * offsets plus rp_tile_count(d)*P*TP, element (i, j) at i*68 + j), so every
+ * 16-column / 16-row slab of a tile is one contiguous block. Entries above the
+ * diagonal of a diagonal tile and the padding are 0; padded diagonal entries
+ * are 1 in plane 0 (the identity) so solves stay well defined. Per fold:
+ * rp_theta_size(d, r) doubles.
  */
 #ifndef RIDGEPATH_B200_H
 #define RIDGEPATH_B200_H
@@ -50,8 +54,10 @@ const char* rp_last_error(void);
 /* Number of kernels this library has launched in the process (evidence for bench.py). */
 long long rp_launch_count(void);
 
-/* Number of 64 x 64 tiles of the packed lower triangle of order d. */
+/* Number of 64 x 64 tiles of the packed lower triangle of order d, and the
+ * size in doubles of one fold's coefficient buffer (both tile copies). */
 int64_t rp_tile_count(int d);
+int64_t rp_theta_size(int d, int r);
 
 /* (1) Hessian blocks.  Replaces ridge.assemble (ridge.py:50-60): H = X^T X
  * (:58-59) and g = X^T y (:60), evaluated per contiguous row block so that
@@ -106,12 +112,14 @@ size_t rp_fit_workspace_size(int d, int nf);
  * linalg.solve_chol (linalg.py:104-128): W[f][:, j*m:(j+1)*m] solves
  * L_f(t_j) L_f(t_j)^T W = rhs[f], with L_f(t) = sum_p theta_p t^p evaluated
  * tile by tile in registers, never materialized.
- *   theta: nf x tile-layout with P = r+1 planes; rhs: nf x (dp x m) row-major
+ *   theta: nf x rp_theta_size(d, r) doubles; rhs: nf x (dp x m) row-major
  *   tvals: q values t_j = t_scale*lambda_j + t_shift (device)
  *   W: nf x (dp x ldw) row-major, ldw >= q*m, ldw even
- *   flags: nf x q ints, set to 1 where min |L_ii(t_j)| < 1e-12              */
+ *   flags: nf x q ints, set to 1 where min |L_ii(t_j)| < 1e-12
+ *   work: rp_eval_solve_workspace_size(d, r, nf, m, q) bytes (per-chunk solve rows) */
+size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int q);
 int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m, const double* tvals,
-                  int q, double* W, int64_t ldw, int* flags, void* stream);
+                  int q, double* W, int64_t ldw, int* flags, void* work, void* stream);
 
 /* Debug / single-lambda API (pichol.eval, pichol.py:154-164): dense d x d
  * column-major L(t) from one fold's tile-layout theta. */

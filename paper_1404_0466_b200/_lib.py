@@ -34,6 +34,7 @@ SIGNATURES = {
     "rp_last_error": (ctypes.c_char_p, []),
     "rp_launch_count": (ctypes.c_longlong, []),
     "rp_tile_count": (_i64, [_i]),
+    "rp_theta_size": (_i64, [_i, _i]),
     "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp]),
     "rp_col_sumsq": (_i, [_vp, _i64, _i64, _i, _i, _vp, _vp]),
     "rp_symmetrize": (_i, [_vp, _i, _i64, _i, _vp]),
@@ -42,7 +43,8 @@ SIGNATURES = {
     "rp_potrf_batched": (_i, [_vp, _i, _i64, _i, _vp, _vp, _vp]),
     "rp_fit_tiles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rp_fit_workspace_size": (_sz, [_i, _i]),
-    "rp_eval_solve": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i64, _vp, _vp]),
+    "rp_eval_solve_workspace_size": (_sz, [_i, _i, _i, _i, _i]),
+    "rp_eval_solve": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i64, _vp, _vp, _vp]),
     "rp_eval_materialize": (_i, [_vp, _i, _i, _d, _vp, _vp]),
     "rp_theta_export": (_i, [_vp, _i, _i, _vp, _i64, _vp, _vp]),
     "rp_theta_import": (_i, [_vp, _i, _i, _vp, _i64, _vp, _vp]),

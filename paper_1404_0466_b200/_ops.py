@@ -88,7 +88,9 @@ def eval_solve(theta_dev, d, r, rhs, tvals):
         ldw = q * mg + ((q * mg) & 1)
         W = _dev.empty((dp, ldw))
         fl = _dev.zeros((q,), dtype=torch.int32)
-        call("rp_eval_solve", ptr(theta_dev), d, r, 1, ptr(R), mg, ptr(dt), q, ptr(W), ldw, ptr(fl), stream())
+        ws = _dev.workspace(_lib.query("rp_eval_solve_workspace_size", d, r, 1, mg, q))
+        call("rp_eval_solve", ptr(theta_dev), d, r, 1, ptr(R), mg, ptr(dt), q, ptr(W), ldw, ptr(fl), ptr(ws),
+             stream())
         Wh = W[:d, : q * mg].cpu().numpy().reshape(d, q, mg)
         out[:, :, c0:c1] = np.transpose(Wh, (1, 0, 2))
         flags |= fl.cpu().numpy()

@@ -89,6 +89,13 @@ RP_DEVINL void named_bar_sync(int id, int threads) {
 
 }  // namespace rp
 
+// Coefficient tile layout v2 (include/ridgepath_b200.h): 64 x 64 planes with a padded leading
+// dimension, stored twice per fold -- column-major ("forward" copy) and row-major (the transposed
+// "backward" copy) -- so that every 16-column / 16-row slab the solve streams is one contiguous
+// bulk copy that lands in the conflict-free padded shared layout.
+constexpr int TILE_LD = 68;
+constexpr int TILE_PLANE = 64 * TILE_LD;
+
 // Status codes of the C ABI (include/ridgepath_b200.h).
 #define RP_OK 0
 #define RP_EINVAL (-1)

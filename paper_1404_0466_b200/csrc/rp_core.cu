@@ -266,6 +266,7 @@ struct FitArgs {
 
 __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles, FitArgs fa, double* theta,
                                  double* partial) {
+  extern __shared__ double pl[];  // P planes of 64 x 65 (column-major, padded) for the transpose
   const int64_t tile = blockIdx.x;
   const int f = blockIdx.y;
   const int P = r + 1;
@@ -275,7 +276,9 @@ __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t n
   const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
   const int64_t n = (int64_t)d * d;
   const double* Lf = L + (int64_t)f * s * n;
-  double* out = theta + ((int64_t)f * ntiles + tile) * P * 4096;
+  const int64_t tsz = (int64_t)P * TILE_PLANE;
+  double* fwd = theta + (int64_t)f * 2 * ntiles * tsz + tile * tsz;
+  double* bwd = fwd + ntiles * tsz;
   double res = 0.0;
   for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
     const int j = e >> 6, i = e & 63;
@@ -288,7 +291,7 @@ __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t n
         double v = 0.0;
         for (int si = 0; si < s; ++si) v = fma(fa.P[p][si], T[si], v);
         th[p] = v;
-        out[p * 4096 + e] = v;
+        pl[p * 4160 + j * 65 + i] = v;
       }
       for (int si = 0; si < s; ++si) {
         double v = 0.0;
@@ -298,8 +301,16 @@ __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t n
       }
     } else {
       const double diag = (row == col && row >= d) ? 1.0 : 0.0;
-      for (int p = 0; p < P; ++p) out[p * 4096 + e] = (p == 0) ? diag : 0.0;
+      for (int p = 0; p < P; ++p) pl[p * 4160 + j * 65 + i] = (p == 0) ? diag : 0.0;
     }
+  }
+  __syncthreads();
+  // forward copy: column-major, leading dimension TILE_LD; backward copy: row-major (transposed)
+  for (int e = threadIdx.x; e < P * TILE_PLANE; e += blockDim.x) {
+    const int p = e / TILE_PLANE, w = e - p * TILE_PLANE;
+    const int a = w / TILE_LD, b = w - a * TILE_LD;  // a: major index, b: minor (0..67)
+    fwd[e] = (b < 64) ? pl[p * 4160 + a * 65 + b] : 0.0;  // (row b, col a)
+    bwd[e] = (b < 64) ? pl[p * 4160 + b * 65 + a] : 0.0;  // (row a, col b)
   }
   __shared__ double red[256];
   red[threadIdx.x] = res;
@@ -327,14 +338,14 @@ __global__ void fit_resid_kernel(const double* partial, int64_t ntiles, double* 
 
 RP_DEVINL int64_t tile_offset(int row, int col, int P) {
   const int I = row >> 6, J = col >> 6;
-  return ((int64_t)I * (I + 1) / 2 + J) * P * 4096 + (col & 63) * 64 + (row & 63);
+  return ((int64_t)I * (I + 1) / 2 + J) * P * TILE_PLANE + (col & 63) * TILE_LD + (row & 63);
 }
 
 // pichol.eval_vector's arithmetic exactly (pichol.py:147-150): v = theta_r; v *= t; v += theta_i,
 // with separate roundings (no FMA contraction).
 RP_DEVINL double horner_ref(const double* th, int P, double t) {
-  double v = th[(int64_t)(P - 1) * 4096];
-  for (int p = P - 2; p >= 0; --p) v = __dadd_rn(__dmul_rn(v, t), th[(int64_t)p * 4096]);
+  double v = th[(int64_t)(P - 1) * TILE_PLANE];
+  for (int p = P - 2; p >= 0; --p) v = __dadd_rn(__dmul_rn(v, t), th[(int64_t)p * TILE_PLANE]);
   return v;
 }
 
@@ -350,30 +361,43 @@ __global__ void export_kernel(const double* theta, int d, int P, const int64_t* 
   if (j >= D) return;
   int64_t pos = perm ? perm[j] : j;
   int row = (int)(pos % d), col = (int)(pos / d);
-  for (int p = 0; p < P; ++p) out[p * D + j] = (row >= col) ? theta[tile_offset(row, col, P) + (int64_t)p * 4096] : 0.0;
+  for (int p = 0; p < P; ++p)
+    out[p * D + j] = (row >= col) ? theta[tile_offset(row, col, P) + (int64_t)p * TILE_PLANE] : 0.0;
 }
 
 __global__ void theta_init_kernel(double* theta, int d, int P, int64_t ntiles) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e >= ntiles * P * 4096) return;
-  int64_t tile = e / (P * 4096);
-  int rem = (int)(e % (P * 4096));
-  int p = rem / 4096, w = rem % 4096;
+  const int64_t half = ntiles * P * TILE_PLANE;
+  if (e >= 2 * half) return;
+  const int64_t w0 = e % half;
+  const int64_t tile = w0 / (P * TILE_PLANE);
+  const int rem = (int)(w0 % (P * TILE_PLANE));
+  const int p = rem / TILE_PLANE, w = rem % TILE_PLANE;
   int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
   while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
   while ((int64_t)I * (I + 1) / 2 > tile) --I;
-  int J = (int)(tile - (int64_t)I * (I + 1) / 2);
-  int row = I * 64 + (w & 63), col = J * 64 + (w >> 6);
-  theta[e] = (p == 0 && row == col && row >= d) ? 1.0 : 0.0;
+  const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  const int mj = w / TILE_LD, mn = w % TILE_LD;
+  // same (row, col) mapping up to transposition; only the padded diagonal is nonzero
+  const int row = I * 64 + mn, col = J * 64 + mj;
+  theta[e] = (p == 0 && mn < 64 && row == col && row >= d) ? 1.0 : 0.0;
 }
 
-__global__ void import_kernel(const double* vec, int d, int P, const int64_t* perm, int64_t D, double* theta) {
+__global__ void import_kernel(const double* vec, int d, int P, const int64_t* perm, int64_t D, int64_t ntiles,
+                              double* theta) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= D) return;
   int64_t pos = perm ? perm[j] : j;
   int row = (int)(pos % d), col = (int)(pos / d);
   if (row < col) return;
-  for (int p = 0; p < P; ++p) theta[tile_offset(row, col, P) + (int64_t)p * 4096] = vec[p * D + j];
+  const int I = row >> 6, J = col >> 6;
+  const int64_t base = ((int64_t)I * (I + 1) / 2 + J) * P * TILE_PLANE;
+  const int64_t half = ntiles * P * TILE_PLANE;
+  for (int p = 0; p < P; ++p) {
+    const double v = vec[p * D + j];
+    theta[base + (int64_t)p * TILE_PLANE + (col & 63) * TILE_LD + (row & 63)] = v;         // forward
+    theta[half + base + (int64_t)p * TILE_PLANE + (row & 63) * TILE_LD + (col & 63)] = v;  // backward
+  }
 }
 
 // ------------------------------------------------------------------ hold-out reductions
@@ -464,6 +488,8 @@ int64_t rp_tile_count(int d) {
   int64_t nt = (d + 63) / 64;
   return nt * (nt + 1) / 2;
 }
+
+int64_t rp_theta_size(int d, int r) { return 2 * rp_tile_count(d) * (r + 1) * TILE_PLANE; }
 
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d, const double* Y,
                    int64_t ldy, int m, double* G, double* C, void* stream) {
@@ -647,7 +673,9 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
     }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nt = rp_tile_count(d);
-  fit_tiles_kernel<<<dim3((unsigned)nt, nf), 256, 0, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
+  const size_t fsm = sizeof(double) * (size_t)(r + 1) * 4160;
+  cudaFuncSetAttribute(fit_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+  fit_tiles_kernel<<<dim3((unsigned)nt, nf), 256, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
   RP_LAUNCH_CHECK("fit_tiles");
   if (resid) {
     fit_resid_kernel<<<nf, 256, 0, st>>>((double*)work, nt, resid);
@@ -673,10 +701,10 @@ int rp_theta_export(const double* theta, int d, int r, const int64_t* perm, int6
 int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_t D, double* theta, void* stream) {
   RP_REQUIRE(d >= 1 && D >= 1 && r >= 0 && r <= 4, "rp_theta_import: bad sizes");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t n = rp_tile_count(d) * (r + 1) * 4096;
+  const int64_t n = rp_theta_size(d, r);
   theta_init_kernel<<<grid1d(n), 256, 0, st>>>(theta, d, r + 1, rp_tile_count(d));
   RP_LAUNCH_CHECK("theta_init");
-  import_kernel<<<grid1d(D), 256, 0, st>>>(vec, d, r + 1, perm, D, theta);
+  import_kernel<<<grid1d(D), 256, 0, st>>>(vec, d, r + 1, perm, D, rp_tile_count(d), theta);
   RP_LAUNCH_CHECK("theta_import");
   return RP_OK;
 }

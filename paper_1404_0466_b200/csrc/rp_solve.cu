@@ -27,50 +27,76 @@ static int launch_generic(int m, const SolveArgs& a, int grid, size_t smem, cuda
   }
 }
 
+struct SolvePlan {
+  int lam = 0, chunks = 0, S = 0, P = 0, nt = 0;
+  bool fast = false;
+  size_t smem = 0;
+};
+
+// Chunk size: specialised kernels (full chunks, compile-time P) and the generic kernel compete
+// on the lowest (waves x chunk) cost, the generic kernel's overhead weighted in.
+static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
+  SolvePlan pl;
+  pl.P = r + 1;
+  pl.nt = (d + 63) / 64;
+  int dev = 0, sms = 148, maxsmem = 227 * 1024;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  double best_cost = 1e300;
+  for (int lam = SOLVE_LC; lam >= 1; --lam) {
+    if (lam * m > 256) continue;  // one thread per (lambda, output) column in the diagonal solve
+    if (solve_smem_bytes(lam, m, pl.P) > (size_t)maxsmem) continue;
+    const int chunks = (q + lam - 1) / lam;
+    const long long ctas = (long long)nf * chunks;
+    const double waves = (double)((ctas + sms - 1) / sms);
+    const double base = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));
+    const bool fast_ok = q >= lam && has_solve_fast(m, pl.P, lam) && ((m % 2 == 0) || ((q - lam) % 2 == 0));
+    const bool gen_ok = lam <= SOLVE_LC_GENERIC && !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks
+    if (fast_ok && base < best_cost - 1e-9) {
+      best_cost = base;
+      pl.lam = lam;
+      pl.fast = true;
+    }
+    if (gen_ok && 2.5 * base < best_cost - 1e-9) {
+      best_cost = 2.5 * base;
+      pl.lam = lam;
+      pl.fast = false;
+    }
+  }
+  if (pl.lam > 0) {
+    pl.chunks = (q + pl.lam - 1) / pl.lam;
+    pl.S = solve_stride(pl.lam, m);
+    pl.smem = solve_smem_bytes(pl.lam, m, pl.P);
+  }
+  return pl;
+}
+
+extern "C" size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int q) {
+  if (d < 1 || nf < 1 || m < 1 || m > 16 || q < 1 || r < 0 || r + 1 > SOLVE_PMAX) return 0;
+  const SolvePlan pl = plan_solve(d, r, nf, m, q);
+  if (pl.lam == 0) return 0;
+  return sizeof(double) * (size_t)nf * pl.chunks * (size_t)pl.nt * 64 * pl.S;
+}
+
 extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m,
-                             const double* tvals, int q, double* W, int64_t ldw, int* flags, void* stream) {
+                             const double* tvals, int q, double* W, int64_t ldw, int* flags, void* work,
+                             void* stream) {
   RP_REQUIRE(d >= 1 && nf >= 1 && q >= 1, "rp_eval_solve: bad sizes d=%d nf=%d q=%d", d, nf, q);
   RP_REQUIRE(r >= 0 && r + 1 <= SOLVE_PMAX, "rp_eval_solve: degree %d outside [0, %d]", r, SOLVE_PMAX - 1);
   RP_REQUIRE(m >= 1 && m <= 16, "rp_eval_solve: %d outputs per call (max 16)", m);
   RP_REQUIRE(ldw >= (int64_t)q * m && ldw % 2 == 0, "rp_eval_solve: ldw=%lld must be even and >= q*m",
              (long long)ldw);
   RP_REQUIRE(((uintptr_t)theta & 15) == 0 && ((uintptr_t)W & 15) == 0, "rp_eval_solve: 16-byte alignment");
+  RP_REQUIRE(work != nullptr && ((uintptr_t)work & 15) == 0, "rp_eval_solve: workspace (16-byte aligned)");
   cudaStream_t st = (cudaStream_t)stream;
-  const int P = r + 1;
-  const int nt = (d + 63) / 64;
-  int dev = 0, sms = 148, maxsmem = 227 * 1024;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  // Candidate chunk sizes: specialised kernels (full chunks, compile-time P) and the generic
-  // kernel; pick the lowest (waves x chunk) cost, weighting the generic kernel's overhead.
-  int best_lam = 0;
-  bool best_fast = false;
-  double best_cost = 1e300;
-  for (int lam = SOLVE_LC; lam >= 1; --lam) {
-    if (lam * m > 256) continue;  // one thread per (lambda, output) column in the diagonal solve
-    if (solve_smem_bytes(lam, m, P) > (size_t)maxsmem) continue;
-    const int chunks = (q + lam - 1) / lam;
-    const long long ctas = (long long)nf * chunks;
-    const double waves = (double)((ctas + sms - 1) / sms);
-    const double base = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));
-    const bool fast_ok = q >= lam && has_solve_fast(m, P, lam) && ((m % 2 == 0) || ((q - lam) % 2 == 0));
-    const bool gen_ok = lam <= SOLVE_LC_GENERIC && !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks
-    if (fast_ok && base < best_cost - 1e-9) {
-      best_cost = base;
-      best_lam = lam;
-      best_fast = true;
-    }
-    if (gen_ok && 2.5 * base < best_cost - 1e-9) {
-      best_cost = 2.5 * base;
-      best_lam = lam;
-      best_fast = false;
-    }
-  }
-  RP_REQUIRE(best_lam >= 1, "rp_eval_solve: no chunk size fits shared memory");
+  const SolvePlan pl = plan_solve(d, r, nf, m, q);
+  RP_REQUIRE(pl.lam >= 1, "rp_eval_solve: no chunk size fits shared memory");
+  const int P = pl.P, nt = pl.nt;
   SolveArgs a;
   a.theta = theta;
-  a.theta_fold_stride = rp_tile_count(d) * P * 4096;
+  a.theta_fold_stride = rp_theta_size(d, r);
+  a.theta_bwd_off = rp_tile_count(d) * P * TILE_PLANE;
   a.rhs = rhs;
   a.rhs_fold_stride = (int64_t)nt * 64 * m;
   a.W = W;
@@ -83,13 +109,13 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   a.d = d;
   a.nt = nt;
   a.P = P;
-  a.lam_per_cta = best_lam;
-  a.chunks = (q + best_lam - 1) / best_lam;
-  a.S = solve_stride(best_lam, m);
-  const size_t smem = solve_smem_bytes(best_lam, m, P);
+  a.lam_per_cta = pl.lam;
+  a.chunks = pl.chunks;
+  a.S = pl.S;
+  a.Wc = (double*)work;
   const int grid = nf * a.chunks;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
   if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");
-  if (best_fast) return launch_solve_fast(m, P, best_lam, a, grid, smem, st);
-  return launch_generic(m, a, grid, smem, st);
+  if (pl.fast) return launch_solve_fast(m, P, pl.lam, a, grid, pl.smem, st);
+  return launch_generic(m, a, grid, pl.smem, st);
 }

@@ -42,6 +42,8 @@ struct SolveArgs {
   const double* tvals;
   int* flags;
   int q, m, d, nt, P, lam_per_cta, chunks, S;
+  double* Wc;             // warp-specialised kernel: chunk-private W rows (dp x S per CTA)
+  int64_t theta_bwd_off;  // offset of the transposed (backward) tile copy inside a fold's theta
 };
 
 RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
@@ -73,7 +75,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   double* sT = smem;
   double* sW = smem + SOLVE_STAGES * stageT;
   const int ring = SOLVE_STAGES * (P * (BWD_SLAB > FWD_SLAB ? BWD_SLAB : FWD_SLAB) + stageW);
-  double* sR = smem + (ring > P * 4096 ? ring : P * 4096);
+  double* sR = smem + (ring > P * TILE_PLANE ? ring : P * TILE_PLANE);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -116,16 +118,16 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         const int st = s % SOLVE_STAGES;
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
         const int kq = s & 3;
-        const double* tile = theta + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * 4096;
+        const double* tile = theta + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
         double* dT = sT + st * stageT;
         for (int c = tid; c < P * 512; c += NTH) {
           const int p = c >> 9, e = c & 511;
           if (!BWD) {
             const int kk = e >> 5, i2 = (e & 31) * 2;  // column kq*16+kk, rows i2, i2+1
-            cp_async16(dT + p * FWD_SLAB + kk * 68 + i2, tile + p * 4096 + (kq * 16 + kk) * 64 + i2, true);
+            cp_async16(dT + p * FWD_SLAB + kk * 68 + i2, tile + p * TILE_PLANE + (kq * 16 + kk) * TILE_LD + i2, true);
           } else {
             const int i = e >> 3, k2 = (e & 7) * 2;  // column i, rows kq*16+k2, +1
-            cp_async16(dT + p * BWD_SLAB + i * 20 + k2, tile + p * 4096 + i * 64 + kq * 16 + k2, true);
+            cp_async16(dT + p * BWD_SLAB + i * 20 + k2, tile + p * TILE_PLANE + i * TILE_LD + kq * 16 + k2, true);
           }
         }
         double* dW = sW + st * stageW;
@@ -200,8 +202,8 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     //      sR, then a triangular solve per (lambda, output) column from shared memory ----
     double* sD = smem;  // union with the ring (idle during the diagonal step)
     {
-      const double* tile = theta + (int64_t)tile_index(I, I) * P * 4096;
-      for (int c = tid; c < P * 2048; c += NTH) cp_async16(sD + 2 * c, tile + 2 * c, true);
+      const double* tile = theta + (int64_t)tile_index(I, I) * P * TILE_PLANE;
+      for (int c = tid; c < P * TILE_PLANE / 2; c += NTH) cp_async16(sD + 2 * c, tile + 2 * c, true);
       cp_async_commit();
     }
     const int rowI = I * 64;
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       auto horner = [&](int off) {
         double c[PM];
 #pragma unroll
-        for (int p = 0; p < PM; ++p) c[p] = (p < P) ? th[p * 4096 + off] : 0.0;
+        for (int p = 0; p < PM; ++p) c[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
         double v = 0.0;
 #pragma unroll
         for (int p = PM - 1; p >= 0; --p)
@@ -265,13 +267,13 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
           int k = 0;
           for (; k + 4 <= i; k += 4) {
-            s0 = fma(horner((k + 0) * 64 + i), x[(k + 0) * S], s0);
-            s1 = fma(horner((k + 1) * 64 + i), x[(k + 1) * S], s1);
-            s2 = fma(horner((k + 2) * 64 + i), x[(k + 2) * S], s2);
-            s3 = fma(horner((k + 3) * 64 + i), x[(k + 3) * S], s3);
+            s0 = fma(horner((k + 0) * TILE_LD + i), x[(k + 0) * S], s0);
+            s1 = fma(horner((k + 1) * TILE_LD + i), x[(k + 1) * S], s1);
+            s2 = fma(horner((k + 2) * TILE_LD + i), x[(k + 2) * S], s2);
+            s3 = fma(horner((k + 3) * TILE_LD + i), x[(k + 3) * S], s3);
           }
-          for (; k < i; ++k) s0 = fma(horner(k * 64 + i), x[k * S], s0);
-          const double lii = horner(i * 64 + i);
+          for (; k < i; ++k) s0 = fma(horner(k * TILE_LD + i), x[k * S], s0);
+          const double lii = horner(i * TILE_LD + i);
           if (rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
           x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
         }
@@ -281,21 +283,24 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
           int k = i + 1;
           for (; k + 4 <= 64; k += 4) {
-            s0 = fma(horner(i * 64 + k + 0), x[(k + 0) * S], s0);
-            s1 = fma(horner(i * 64 + k + 1), x[(k + 1) * S], s1);
-            s2 = fma(horner(i * 64 + k + 2), x[(k + 2) * S], s2);
-            s3 = fma(horner(i * 64 + k + 3), x[(k + 3) * S], s3);
+            s0 = fma(horner(i * TILE_LD + k + 0), x[(k + 0) * S], s0);
+            s1 = fma(horner(i * TILE_LD + k + 1), x[(k + 1) * S], s1);
+            s2 = fma(horner(i * TILE_LD + k + 2), x[(k + 2) * S], s2);
+            s3 = fma(horner(i * TILE_LD + k + 3), x[(k + 3) * S], s3);
           }
-          for (; k < 64; ++k) s0 = fma(horner(i * 64 + k), x[k * S], s0);
-          const double lii = horner(i * 64 + i);
+          for (; k < 64; ++k) s0 = fma(horner(i * TILE_LD + k), x[k * S], s0);
+          const double lii = horner(i * TILE_LD + i);
           x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
         }
       }
     }
     __syncthreads();
+    // a full chunk that overlaps its neighbour (LCT > 0) writes only the columns it owns, so the
+    // neighbour's backward pass never reads a column already overwritten here
+    const int own0 = LCT ? (chunk * LCT - l0) * m : 0;
     for (int i = warp; i < 64; i += NTH / 32) {
       double* dst = W + (int64_t)(rowI + i) * a.ldw + wcol0;
-      for (int c = lane; c < cw; c += 32) dst[c] = sR[i * S + c];
+      for (int c = own0 + lane; c < cw; c += 32) dst[c] = sR[i * S + c];
     }
     __syncthreads();
   }
@@ -307,7 +312,7 @@ inline size_t solve_smem_bytes(int lam, int m, int P) {
   const int S = solve_stride(lam, m);
   size_t per_stage = (size_t)P * (BWD_SLAB > FWD_SLAB ? BWD_SLAB : FWD_SLAB) + 16 * (size_t)S;
   size_t ring = SOLVE_STAGES * per_stage;
-  size_t diag = (size_t)P * 4096;  // theta_II staged into the idle ring during the diagonal step
+  size_t diag = (size_t)P * TILE_PLANE;  // theta_II staged into the idle ring during the diagonal step
   return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S);
 }
 

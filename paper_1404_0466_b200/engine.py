@@ -41,8 +41,8 @@ def padded(d):
 
 
 def tile_elems(d, P):
-    nt = (d + TILE - 1) // TILE
-    return nt * (nt + 1) // 2 * P * TILE * TILE
+    """Doubles of one fold's coefficient buffer (both tile copies, include/ridgepath_b200.h)."""
+    return int(_lib.query("rp_theta_size", d, P - 1))
 
 
 class PicholEngine:
@@ -120,6 +120,8 @@ class PicholEngine:
         nval = max(self.block_rows[f] for f in self.local_folds)
         mg = max(c1 - c0 for c0, c1 in self.groups)
         self.ws_hold = torch.empty((_lib.query("rp_holdout_workspace_size", nval, d, q, mg, 1 if not self.equal_blocks else nf),), **u8)
+        self.ws_solve = torch.empty((max(_lib.query("rp_eval_solve_workspace_size", d, self.r, nf, c1 - c0, q)
+                                         for c0, c1 in self.groups),), **u8)
 
     def device_bytes(self):
         tot = 0
@@ -177,7 +179,7 @@ class PicholEngine:
                 self.rhs_g[gi].copy_(self.rhs[:, :, c0:c1])
             W = self.W[gi]
             call("rp_eval_solve", ptr(self.theta), self.d, self.r, self.nf, ptr(self.rhs_g[gi]), c1 - c0,
-                 ptr(self.tvals), self.q, ptr(W), W.shape[2], ptr(self.flags[gi]), stream())
+                 ptr(self.tvals), self.q, ptr(W), W.shape[2], ptr(self.flags[gi]), ptr(self.ws_solve), stream())
 
     def stage_holdout(self, X, Y):
         st = stream()

@@ -43,9 +43,9 @@ def test_library_queries_without_gpu():
 def test_invalid_arguments_map_to_usage_errors():
     # validation happens before any CUDA call, so this runs on the CPU box
     with pytest.raises(errors.DimensionMismatch):
-        _lib.call("rp_eval_solve", None, 0, 2, 1, None, 1, None, 1, None, 2, None, None)
+        _lib.call("rp_eval_solve", None, 0, 2, 1, None, 1, None, 1, None, 2, None, None, None)
     with pytest.raises(errors.UsageError):
-        _lib.call("rp_eval_solve", None, 64, 9, 1, None, 1, None, 1, None, 2, None, None)
+        _lib.call("rp_eval_solve", None, 64, 9, 1, None, 1, None, 1, None, 2, None, None, None)
     with pytest.raises(errors.UsageError):
         _lib.call("rp_potrf_batched", None, 0, 0, 1, None, None, None)
     assert "rp_potrf_batched" in _lib.last_error()
