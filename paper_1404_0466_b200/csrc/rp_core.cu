@@ -264,8 +264,9 @@ struct FitArgs {
   double V[32][5];  // s x (r+1)
 };
 
-__global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles, FitArgs fa, double* theta,
-                                 double* partial) {
+template <int SMAX>
+__global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles,
+                                                        FitArgs fa, double* theta, double* partial) {
   extern __shared__ double pl[];  // P planes of 64 x 65 (column-major, padded) for the transpose
   const int64_t tile = blockIdx.x;
   const int f = blockIdx.y;
@@ -284,20 +285,31 @@ __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t n
     const int j = e >> 6, i = e & 63;
     const int row = I * 64 + i, col = J * 64 + j;
     if (row < d && col < d && row >= col) {
-      double T[32];
-      for (int si = 0; si < s; ++si) T[si] = Lf[si * n + (int64_t)col * d + row];
+      double T[SMAX];
+#pragma unroll
+      for (int si = 0; si < SMAX; ++si) T[si] = (si < s) ? __ldcs(Lf + si * n + (int64_t)col * d + row) : 0.0;
       double th[5];
-      for (int p = 0; p < P; ++p) {
-        double v = 0.0;
-        for (int si = 0; si < s; ++si) v = fma(fa.P[p][si], T[si], v);
-        th[p] = v;
-        pl[p * 4160 + j * 65 + i] = v;
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        if (p < P) {
+          double v = 0.0;
+#pragma unroll
+          for (int si = 0; si < SMAX; ++si)
+            if (si < s) v = fma(fa.P[p][si], T[si], v);
+          th[p] = v;
+          pl[p * 4160 + j * 65 + i] = v;
+        }
       }
-      for (int si = 0; si < s; ++si) {
-        double v = 0.0;
-        for (int p = 0; p < P; ++p) v = fma(fa.V[si][p], th[p], v);
-        double dlt = T[si] - v;
-        res = fma(dlt, dlt, res);
+#pragma unroll
+      for (int si = 0; si < SMAX; ++si) {
+        if (si < s) {
+          double v = 0.0;
+#pragma unroll
+          for (int p = 0; p < 5; ++p)
+            if (p < P) v = fma(fa.V[si][p], th[p], v);
+          const double dlt = T[si] - v;
+          res = fma(dlt, dlt, res);
+        }
       }
     } else {
       const double diag = (row == col && row >= d) ? 1.0 : 0.0;
@@ -309,13 +321,13 @@ __global__ void fit_tiles_kernel(const double* L, int d, int s, int r, int64_t n
   for (int e = threadIdx.x; e < P * TILE_PLANE; e += blockDim.x) {
     const int p = e / TILE_PLANE, w = e - p * TILE_PLANE;
     const int a = w / TILE_LD, b = w - a * TILE_LD;  // a: major index, b: minor (0..67)
-    fwd[e] = (b < 64) ? pl[p * 4160 + a * 65 + b] : 0.0;  // (row b, col a)
-    bwd[e] = (b < 64) ? pl[p * 4160 + b * 65 + a] : 0.0;  // (row a, col b)
+    __stcs(fwd + e, (b < 64) ? pl[p * 4160 + a * 65 + b] : 0.0);  // (row b, col a)
+    __stcs(bwd + e, (b < 64) ? pl[p * 4160 + b * 65 + a] : 0.0);  // (row a, col b)
   }
-  __shared__ double red[256];
+  __shared__ double red[512];
   red[threadIdx.x] = res;
   __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
@@ -674,8 +686,13 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nt = rp_tile_count(d);
   const size_t fsm = sizeof(double) * (size_t)(r + 1) * 4160;
-  cudaFuncSetAttribute(fit_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-  fit_tiles_kernel<<<dim3((unsigned)nt, nf), 256, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
+  if (s <= 8) {
+    cudaFuncSetAttribute(fit_tiles_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
+  } else {
+    cudaFuncSetAttribute(fit_tiles_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
+  }
   RP_LAUNCH_CHECK("fit_tiles");
   if (resid) {
     fit_resid_kernel<<<nf, 256, 0, st>>>((double*)work, nt, resid);

@@ -230,6 +230,7 @@ class CvSession:
         self.tvals = _dev.to_dev(self.t_scale * grid_values + self.t_shift)
         self._exchange = None
         self._gather = None
+        self._copy_stream = None
         if shard is not None and shard.world > 1:
             self._exchange = lambda e: dist.exchange_grams(shard, e.G, e.C, e.yy)
             self._gather = lambda c: dist.gather_curves(shard, c)
@@ -252,15 +253,52 @@ class CvSession:
             else:
                 dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64).reshape(dst.shape)))
 
-    def sweep(self, timings=None):
+    def upload_streamed(self, X, Y):
+        """Copy pinned host X/Y fold block by fold block on a side stream; returns the per-block
+        events the Gram stage waits on (the copy of block b+1 overlaps the Gram of block b)."""
+        import torch
+
+        eng = self.engine
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream()
+        cs = self._copy_stream
+        cs.wait_stream(torch.cuda.current_stream())  # previous users of X/Y are done
+        ready = {}
+        with torch.cuda.stream(cs):
+            self.Y.copy_(Y.reshape(self.Y.shape), non_blocking=True)
+            order = eng.gram_blocks + [b for b in range(eng.k) if b not in eng.gram_blocks]
+            for b in order:
+                lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
+                self.X[lo:hi].copy_(X[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                ready[b] = ev
+        # later stages (hold-out of local folds) read all of X: order them after the last copy
+        self._all_copied = ev
+        return ready
+
+    def sweep(self, timings=None, block_ready=None):
         """Device-only sweep on the resident X/Y; returns device (curves, mean, best)."""
         return self.engine.sweep(self.X, self.Y, self.lams, self.P, self.V, self.tvals,
-                                 exchange_grams=self._exchange, gather_curves=self._gather, timings=timings)
+                                 exchange_grams=self._exchange, gather_curves=self._gather, timings=timings,
+                                 block_ready=block_ready)
 
     def run(self, X, Y, timings=None):
-        """Host in, host out: (curves (k, q, m), best index (m,)) as numpy."""
-        self.upload(X, Y)
-        curves, _, best = self.sweep(timings)
+        """Host in, host out: (curves (k, q, m), best index (m,)) as numpy.
+
+        Pinned torch tensors are streamed in per fold block, overlapped with the Gram stage."""
+        import torch
+
+        pinned = isinstance(X, torch.Tensor) and X.is_pinned() and isinstance(Y, torch.Tensor) and Y.is_pinned()
+        if pinned:
+            ready = self.upload_streamed(X, Y)
+            Xd = self.X
+            curves, _, best = self.engine.sweep(Xd, self.Y, self.lams, self.P, self.V, self.tvals,
+                                                exchange_grams=self._exchange, gather_curves=self._gather,
+                                                timings=timings, block_ready=ready)
+        else:
+            self.upload(X, Y)
+            curves, _, best = self.sweep(timings)
         bad = self.engine.check_numerics(self.lams)
         if bad is not None:
             f, j = bad

@@ -133,12 +133,14 @@ class PicholEngine:
         return tot
 
     # ------------------------------------------------------------------ stages
-    def stage_gram(self, X, Y):
+    def stage_gram(self, X, Y, block_ready=None):
+        """Gram blocks. block_ready: optional {block: cuda.Event} -- the Gram of a block then waits
+        only for that block's upload, so the host->device copy of later blocks overlaps it."""
         d, m = self.d, self.m
         st = stream()
         blocks = self.gram_blocks
         contiguous = blocks == list(range(blocks[0], blocks[0] + len(blocks)))
-        if self.equal_blocks and contiguous:
+        if self.equal_blocks and contiguous and block_ready is None:
             b0 = blocks[0]
             rows = self.block_rows[0]
             off = int(self.row_off[b0])
@@ -147,7 +149,10 @@ class PicholEngine:
             if self.holdout == "gram":
                 call("rp_col_sumsq", ptr(Y[off:]), m, rows, len(blocks), m, ptr(self.yy[b0]), st)
         else:
+            cur = self.torch.cuda.current_stream()
             for b in blocks:
+                if block_ready is not None:
+                    cur.wait_event(block_ready[b])
                 off, rows = int(self.row_off[b]), self.block_rows[b]
                 call("rp_gram_blocks", ptr(X[off:]), d, rows, 1, d, ptr(Y[off:]), m, m,
                      ptr(self.G[b]), ptr(self.C[b]), st)
@@ -228,7 +233,7 @@ class PicholEngine:
 
     # ------------------------------------------------------------------ sweep
     def sweep(self, X, Y, sample_lams, Pmat, Vmat, tvals, exchange_grams=None, gather_curves=None,
-              timings=None):
+              timings=None, block_ready=None):
         """Run stages (1)-(6). X: (n, d), Y: (n, m) float64 CUDA, rows grouped by fold block.
         tvals: (q,) host or device t values. Returns (curves_all, mean, best) device tensors."""
         torch = self.torch
@@ -245,7 +250,10 @@ class PicholEngine:
                 ev.append((name, e))
 
         mark("start")
-        self.stage_gram(X, Y)
+        self.stage_gram(X, Y, block_ready)
+        if block_ready is not None:  # later stages may read any row of X / Y
+            for done in block_ready.values():
+                torch.cuda.current_stream().wait_event(done)
         if exchange_grams is not None:
             exchange_grams(self)
         self.stage_systems(sample_lams)
