@@ -142,9 +142,11 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     issue(0);
     issue(1);
     for (int s = 0; s < nslab; ++s) {
-      issue(s + 2);
-      cp_async_wait<2>();
+      // one barrier per slab: after it, slab s has landed for everybody and every warp has
+      // finished slab s-1, so its stage ((s + 2) % 3) can be refilled
+      cp_async_wait<1>();
       __syncthreads();
+      issue(s + 2);
       const double* T = sT + (s % SOLVE_STAGES) * stageT;
       const double* Wb = sW + (s % SOLVE_STAGES) * stageW;
 #pragma unroll
@@ -193,7 +195,6 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           }
         }
       }
-      __syncthreads();
     }
     cp_async_wait<0>();
     __syncthreads();

@@ -44,7 +44,10 @@ static int ws_pass(const SolveArgs& a, int grid, cudaStream_t st, size_t maxsmem
 
 template <int M, int P, int LC>
 static int launch_fast(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
-  if (!g_solve_ws) return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG>(a, grid, smem, st);
+  if (!g_solve_ws) {
+    // 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4
+    return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG>(a, grid, smem, st);
+  }
   int dev = 0, maxsmem = 227 * 1024;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsmem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
