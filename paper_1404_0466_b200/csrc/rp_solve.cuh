@@ -246,54 +246,57 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     cp_async_wait<0>();
     __syncthreads();
-    if (tid < cw) {
-      const int l = tid / m, col = tid - (tid / m) * m;
+    // triangular solve of the 64 x 64 diagonal tile: 4 lanes per (lambda, output) column split
+    // every dot product (k = t4 mod 4) and combine it with two shuffles, so all warps take part
+    for (int c0 = 0; c0 < cw; c0 += NTH / 4) {
+      const int c = c0 + (tid >> 2), t4 = tid & 3;
+      const bool live = c < cw;
+      const int cc = live ? c : cw - 1;
+      const int l = cc / m;
       const double tv = a.tvals[l0 + l];
       const double* th = sD;
-      double* x = sR + l * m + col;
+      double* x = sR + cc;
       // all threads read the same coefficient address at the same time -> smem broadcast
       auto horner = [&](int off) {
-        double c[PM];
+        double cf[PM];
 #pragma unroll
-        for (int p = 0; p < PM; ++p) c[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
+        for (int p = 0; p < PM; ++p) cf[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
         double v = 0.0;
 #pragma unroll
         for (int p = PM - 1; p >= 0; --p)
-          if (p < P) v = (p == P - 1) ? c[p] : fma(v, tv, c[p]);
+          if (p < P) v = (p == P - 1) ? cf[p] : fma(v, tv, cf[p]);
         return v;
       };
-      if (!BWD) {
-        bool singular = false;
-        for (int i = 0; i < 64; ++i) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int k = 0;
-          for (; k + 4 <= i; k += 4) {
-            s0 = fma(horner((k + 0) * TILE_LD + i), x[(k + 0) * S], s0);
-            s1 = fma(horner((k + 1) * TILE_LD + i), x[(k + 1) * S], s1);
-            s2 = fma(horner((k + 2) * TILE_LD + i), x[(k + 2) * S], s2);
-            s3 = fma(horner((k + 3) * TILE_LD + i), x[(k + 3) * S], s3);
+      bool singular = false;
+      for (int s = 0; s < 64; ++s) {
+        const int i = BWD ? 63 - s : s;
+        double p0 = 0.0, p1 = 0.0;
+        if (!BWD) {
+          int k = t4;
+          for (; k + 4 < i; k += 8) {
+            p0 = fma(horner(k * TILE_LD + i), x[k * S], p0);
+            p1 = fma(horner((k + 4) * TILE_LD + i), x[(k + 4) * S], p1);
           }
-          for (; k < i; ++k) s0 = fma(horner(k * TILE_LD + i), x[k * S], s0);
-          const double lii = horner(i * TILE_LD + i);
-          if (rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
-          x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
-        }
-        if (singular && col == 0) a.flags[fold * a.q + l0 + l] = 1;
-      } else {
-        for (int i = 63; i >= 0; --i) {
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-          int k = i + 1;
-          for (; k + 4 <= 64; k += 4) {
-            s0 = fma(horner(i * TILE_LD + k + 0), x[(k + 0) * S], s0);
-            s1 = fma(horner(i * TILE_LD + k + 1), x[(k + 1) * S], s1);
-            s2 = fma(horner(i * TILE_LD + k + 2), x[(k + 2) * S], s2);
-            s3 = fma(horner(i * TILE_LD + k + 3), x[(k + 3) * S], s3);
+          if (k < i) p0 = fma(horner(k * TILE_LD + i), x[k * S], p0);
+        } else {
+          int k = i + 1 + ((t4 - (i + 1)) & 3);  // first k > i with k = t4 mod 4
+          for (; k + 4 < 64; k += 8) {
+            p0 = fma(horner(i * TILE_LD + k), x[k * S], p0);
+            p1 = fma(horner(i * TILE_LD + k + 4), x[(k + 4) * S], p1);
           }
-          for (; k < 64; ++k) s0 = fma(horner(i * TILE_LD + k), x[k * S], s0);
-          const double lii = horner(i * TILE_LD + i);
-          x[i * S] = (x[i * S] - ((s0 + s1) + (s2 + s3))) / lii;
+          if (k < 64) p0 = fma(horner(i * TILE_LD + k), x[k * S], p0);
         }
+        double part = p0 + p1;
+        part += __shfl_xor_sync(0xffffffffu, part, 1);
+        part += __shfl_xor_sync(0xffffffffu, part, 2);
+        const double lii = horner(i * TILE_LD + i);
+        if (!BWD && rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
+        const double xi = (x[i * S] - part) / lii;
+        __syncwarp();
+        if (t4 == 0 && live) x[i * S] = xi;
+        __syncwarp();
       }
+      if (!BWD && singular && live && t4 == 0 && (c % m) == 0) a.flags[fold * a.q + l0 + l] = 1;
     }
     __syncthreads();
     // a full chunk that overlaps its neighbour (LCT > 0) writes only the columns it owns, so the
@@ -307,7 +310,10 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   }
 }
 
-inline int solve_stride(int lam, int m) { return ((lam * m + 7) / 16) * 16 + 8; }
+// Row stride of the W / R tiles: >= lam*m and = 12 (mod 16) doubles, so the DMMA B fragments
+// (rows t, cols g) and the 16-byte leftover-column loads (4 rows, one address per row) are both
+// bank-conflict free.
+inline int solve_stride(int lam, int m) { return ((lam * m + 3) / 16) * 16 + 12; }
 
 inline size_t solve_smem_bytes(int lam, int m, int P) {
   const int S = solve_stride(lam, m);
