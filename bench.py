@@ -77,6 +77,18 @@ def peaks():
     return out
 
 
+def ncu_traffic(stage):
+    """DRAM bytes (read + write) per launch of a stage's main kernel from the committed
+    `ncu --set full` capture (profiles/r01_ncu_top_kernels.json), else None."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_top_kernels.json")
+    key = {"gram": "gram_syrk"}.get(stage)
+    if key is None or not os.path.exists(p):
+        return None
+    with open(p) as f:
+        k = json.load(f).get(key)
+    return None if k is None else k["dram_read_bytes"] + k["dram_write_bytes"]
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -320,8 +332,8 @@ def run_ours(args, cfg, world, rank, local):
     dom = max(stages, key=lambda s: stages[s]["ms"])
     nf = len(shard.local_folds)
     roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
-            "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": None,
-            "peak_src": pk["fp64_src"], "algorithmic_flops": flops[dom] }
+            "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": ncu_traffic(dom),
+            "peak_src": pk["fp64_src"], "algorithmic_flops": flops[dom]}
     stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9 if "solve" in stages else None
 
     out = {
