@@ -1,6 +1,8 @@
 // (5) Fused evaluate + solve: host dispatch of rp_eval_solve and the generic (runtime P and
 // chunk size) kernel instantiations. The kernel itself is in rp_solve.cuh; the specialised
 // (compile-time P and chunk) instantiations used by the BASELINE configs are in rp_solve_fast.cu.
+#include <cstdlib>
+
 #include "rp_solve.cuh"
 #include "../../include/ridgepath_b200.h"
 
@@ -113,6 +115,11 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   a.chunks = pl.chunks;
   a.S = pl.S;
   a.Wc = (double*)work;
+  static const int dbg = [] {
+    const char* e = getenv("RP_SOLVE_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  a.dbg = dbg;
   const int grid = nf * a.chunks;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
   if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");

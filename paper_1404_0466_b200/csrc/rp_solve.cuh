@@ -42,6 +42,7 @@ struct SolveArgs {
   const double* tvals;
   int* flags;
   int q, m, d, nt, P, lam_per_cta, chunks, S;
+  int dbg;  // experiments only (RP_SOLVE_DBG): 1 = skip slab copies, 2 = skip diagonal solves
   double* Wc;             // warp-specialised kernel: chunk-private W rows (dp x S per CTA)
   int64_t theta_bwd_off;  // offset of the transposed (backward) tile copy inside a fold's theta
 };
@@ -66,16 +67,16 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   constexpr int REMA = REM > 0 ? REM : 1;
   constexpr int NTA = NT > 0 ? NT : 1;
   constexpr bool REM2 = (REM % 2) == 0;
-  constexpr int SLAB = BWD ? BWD_SLAB : FWD_SLAB;
   extern __shared__ __align__(16) double smem[];
   const int P = PT ? PT : a.P;
   const int S = a.S, m = a.m;
-  const int stageT = P * SLAB;
+  const int stageT = P * FWD_SLAB;  // both directions: [k][68] slabs (bwd from the transposed copy)
   const int stageW = 16 * S;
   double* sT = smem;
   double* sW = smem + SOLVE_STAGES * stageT;
-  const int ring = SOLVE_STAGES * (P * (BWD_SLAB > FWD_SLAB ? BWD_SLAB : FWD_SLAB) + stageW);
+  const int ring = SOLVE_STAGES * (stageT + stageW);
   double* sR = smem + (ring > P * TILE_PLANE ? ring : P * TILE_PLANE);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sR + 64 * S);  // per stage, + [3] diagonal tile
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -85,10 +86,17 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
   if (nl <= 0) return;
   const double* theta = a.theta + fold * a.theta_fold_stride;
+  const double* thslab = theta + (BWD ? a.theta_bwd_off : 0);  // slabs: fwd or transposed copy
   double* W = a.W + fold * a.w_fold_stride;
-  const int cw = nl * m;             // valid chunk columns
-  const int cpairs = (cw + 1) >> 1;  // 16-byte copies per W row
+  double* Wc = a.Wc + (int64_t)blockIdx.x * (a.nt * 64) * S;  // this CTA's private solve rows
+  const int cw = nl * m;  // valid chunk columns
   const int64_t wcol0 = (int64_t)l0 * m;
+  if (tid == 0) {
+    for (int i = 0; i <= SOLVE_STAGES; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  int it0 = 0;  // slabs consumed by earlier rows (stage / phase bookkeeping)
 
   double tl[LH];
 #pragma unroll
@@ -113,42 +121,34 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         for (int c = 0; c < REMA; ++c) accx[i][mt][c] = 0.0;
       }
 
+    // one thread streams slab s: P contiguous 16-column (fwd) / 16-row (bwd, transposed copy)
+    // plane slices + the 16 already solved rows of this CTA's private W, completion on full[st]
     auto issue = [&](int s) {
-      if (s < nslab) {
-        const int st = s % SOLVE_STAGES;
+      if (tid == 0 && s < nslab && !(a.dbg & 1)) {
+        const int st = (it0 + s) % SOLVE_STAGES;
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
         const int kq = s & 3;
-        const double* tile = theta + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
-        double* dT = sT + st * stageT;
-        for (int c = tid; c < P * 512; c += NTH) {
-          const int p = c >> 9, e = c & 511;
-          if (!BWD) {
-            const int kk = e >> 5, i2 = (e & 31) * 2;  // column kq*16+kk, rows i2, i2+1
-            cp_async16(dT + p * FWD_SLAB + kk * 68 + i2, tile + p * TILE_PLANE + (kq * 16 + kk) * TILE_LD + i2, true);
-          } else {
-            const int i = e >> 3, k2 = (e & 7) * 2;  // column i, rows kq*16+k2, +1
-            cp_async16(dT + p * BWD_SLAB + i * 20 + k2, tile + p * TILE_PLANE + i * TILE_LD + kq * 16 + k2, true);
-          }
-        }
-        double* dW = sW + st * stageW;
-        const double* src = W + (int64_t)(J * 64 + kq * 16) * a.ldw + wcol0;
-        for (int kk = warp; kk < 16; kk += NTH / 32)
-          for (int c2 = 2 * lane; c2 < 2 * cpairs; c2 += 64)
-            cp_async16(dW + kk * S + c2, src + (int64_t)kk * a.ldw + c2, true);
+        const double* tile = thslab + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
+        const uint32_t bytes = (uint32_t)(P * FWD_SLAB * 8 + 16 * S * 8);
+        mbar_arrive_expect_tx(&full[st], bytes);
+        for (int p = 0; p < P; ++p)
+          bulk_g2s(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
+                   (uint32_t)(FWD_SLAB * 8), &full[st]);
+        bulk_g2s(sW + st * stageW, Wc + (int64_t)(J * 64 + kq * 16) * S, (uint32_t)(16 * S * 8), &full[st]);
       }
-      cp_async_commit();
     };
 
     issue(0);
     issue(1);
     for (int s = 0; s < nslab; ++s) {
-      // one barrier per slab: after it, slab s has landed for everybody and every warp has
-      // finished slab s-1, so its stage ((s + 2) % 3) can be refilled
-      cp_async_wait<1>();
+      // one barrier per slab: after it every warp has finished slab s-1, so its stage can be
+      // refilled with slab s+2; then wait for slab s's bytes
       __syncthreads();
       issue(s + 2);
-      const double* T = sT + (s % SOLVE_STAGES) * stageT;
-      const double* Wb = sW + (s % SOLVE_STAGES) * stageW;
+      const int st = (it0 + s) % SOLVE_STAGES;
+      if (!(a.dbg & 1)) mbar_wait(&full[st], ((it0 + s) / SOLVE_STAGES) & 1);
+      const double* T = sT + st * stageT;
+      const double* Wb = sW + st * stageW;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         const int k = ks * 4 + t;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           const int row = rg * 16 + mt * 8 + g;
 #pragma unroll
           for (int p = 0; p < PM; ++p)
-            if (p < P) th[mt][p] = BWD ? T[p * BWD_SLAB + row * 20 + k] : T[p * FWD_SLAB + k * 68 + row];
+            if (p < P) th[mt][p] = T[p * FWD_SLAB + k * 68 + row];
         }
         const double* wrow = Wb + k * S;
 #pragma unroll
@@ -196,16 +196,16 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
     }
-    cp_async_wait<0>();
-    __syncthreads();
+    it0 += nslab;
+    __syncthreads();  // every warp is done with the ring
 
-    // ---- diagonal tile: stage theta_II (P x 64 x 64) into the drained ring, R = base - acc into
-    //      sR, then a triangular solve per (lambda, output) column from shared memory ----
+    // ---- diagonal tile: stage theta_II (P x 64 x 64, forward copy) into the drained ring,
+    //      R = base - acc into sR, then a triangular solve per (lambda, output) column ----
     double* sD = smem;  // union with the ring (idle during the diagonal step)
-    {
+    if (tid == 0) {
       const double* tile = theta + (int64_t)tile_index(I, I) * P * TILE_PLANE;
-      for (int c = tid; c < P * TILE_PLANE / 2; c += NTH) cp_async16(sD + 2 * c, tile + 2 * c, true);
-      cp_async_commit();
+      mbar_arrive_expect_tx(&full[SOLVE_STAGES], (uint32_t)(P * TILE_PLANE * 8));
+      bulk_g2s(sD, tile, (uint32_t)(P * TILE_PLANE * 8), &full[SOLVE_STAGES]);
     }
     const int rowI = I * 64;
 #pragma unroll
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               const int col = j * 8 + 2 * t + h;
-              double base = BWD ? W[(int64_t)(rowI + row) * a.ldw + wcol0 + l * m + col]
+              double base = BWD ? Wc[(int64_t)(rowI + row) * S + l * m + col]
                                 : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + row) * m + col];
               sR[row * S + l * m + col] = base - acc[i][mt][j][h];
             }
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 #pragma unroll
             for (int c = 0; c < REM; ++c) {
               const int col = NT * 8 + c;
-              double base = BWD ? W[(int64_t)(rowI + row) * a.ldw + wcol0 + l * m + col]
+              double base = BWD ? Wc[(int64_t)(rowI + row) * S + l * m + col]
                                 : a.rhs[fold * a.rhs_fold_stride + (int64_t)(rowI + row) * m + col];
               sR[row * S + l * m + col] = base - accx[i][mt][c];
             }
@@ -244,11 +244,11 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
     }
-    cp_async_wait<0>();
+    mbar_wait(&full[SOLVE_STAGES], step & 1);
     __syncthreads();
     // triangular solve of the 64 x 64 diagonal tile: 4 lanes per (lambda, output) column split
     // every dot product (k = t4 mod 4) and combine it with two shuffles, so all warps take part
-    for (int c0 = 0; c0 < cw; c0 += NTH / 4) {
+    for (int c0 = 0; c0 < ((a.dbg & 2) ? 0 : cw); c0 += NTH / 4) {
       const int c = c0 + (tid >> 2), t4 = tid & 3;
       const bool live = c < cw;
       const int cc = live ? c : cw - 1;
@@ -299,13 +299,17 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       if (!BWD && singular && live && t4 == 0 && (c % m) == 0) a.flags[fold * a.q + l0 + l] = 1;
     }
     __syncthreads();
-    // a full chunk that overlaps its neighbour (LCT > 0) writes only the columns it owns, so the
-    // neighbour's backward pass never reads a column already overwritten here
-    const int own0 = LCT ? (chunk * LCT - l0) * m : 0;
+    // publish row I: private rows (read back by later slabs through the async proxy) and, for
+    // the backward pass, the caller's row-major W (overlapping chunks write identical values)
     for (int i = warp; i < 64; i += NTH / 32) {
-      double* dst = W + (int64_t)(rowI + i) * a.ldw + wcol0;
-      for (int c = own0 + lane; c < cw; c += 32) dst[c] = sR[i * S + c];
+      double* dc = Wc + (int64_t)(rowI + i) * S;
+      for (int c = lane; c < cw; c += 32) dc[c] = sR[i * S + c];
+      if (BWD) {
+        double* dst = W + (int64_t)(rowI + i) * a.ldw + wcol0;
+        for (int c = lane; c < cw; c += 32) dst[c] = sR[i * S + c];
+      }
     }
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
     __syncthreads();
   }
 }
@@ -317,10 +321,10 @@ inline int solve_stride(int lam, int m) { return ((lam * m + 3) / 16) * 16 + 12;
 
 inline size_t solve_smem_bytes(int lam, int m, int P) {
   const int S = solve_stride(lam, m);
-  size_t per_stage = (size_t)P * (BWD_SLAB > FWD_SLAB ? BWD_SLAB : FWD_SLAB) + 16 * (size_t)S;
+  size_t per_stage = (size_t)P * FWD_SLAB + 16 * (size_t)S;
   size_t ring = SOLVE_STAGES * per_stage;
   size_t diag = (size_t)P * TILE_PLANE;  // theta_II staged into the idle ring during the diagonal step
-  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S);
+  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 8);  // + mbarriers
 }
 
 
