@@ -246,59 +246,132 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     mbar_wait(&full[SOLVE_STAGES], step & 1);
     __syncthreads();
-    // triangular solve of the 64 x 64 diagonal tile: 4 lanes per (lambda, output) column split
-    // every dot product (k = t4 mod 4) and combine it with two shuffles, so all warps take part
-    for (int c0 = 0; c0 < ((a.dbg & 2) ? 0 : cw); c0 += NTH / 4) {
-      const int c = c0 + (tid >> 2), t4 = tid & 3;
-      const bool live = c < cw;
-      const int cc = live ? c : cw - 1;
-      const int l = cc / m;
-      const double tv = a.tvals[l0 + l];
-      const double* th = sD;
-      double* x = sR + cc;
-      // all threads read the same coefficient address at the same time -> smem broadcast
-      auto horner = [&](int off) {
-        double cf[PM];
+    // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows: each 16 x 16 diagonal
+    // block is solved with 4 lanes per (lambda, output) column (k = t4 mod 4 split, two shuffles);
+    // the block's contribution to the remaining rows is then applied with DMMA like a slab
+    // (A = L(rows, block cols) evaluated from sD, B = the block's solved rows in sR).
+    bool singular_any = false;
+    for (int q = 0; q < 4; ++q) {
+      const int sb = BWD ? 3 - q : q;
+      const int r0 = sb * 16;
+      for (int c0 = 0; c0 < ((a.dbg & 2) ? 0 : cw); c0 += NTH / 4) {
+        const int c = c0 + (tid >> 2), t4 = tid & 3;
+        const bool live = c < cw;
+        const int cc = live ? c : cw - 1;
+        const int l = cc / m;
+        const double tv = a.tvals[l0 + l];
+        const double* th = sD;
+        double* x = sR + cc;
+        // all threads read the same coefficient address at the same time -> smem broadcast
+        auto horner = [&](int off) {
+          double cf[PM];
 #pragma unroll
-        for (int p = 0; p < PM; ++p) cf[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
-        double v = 0.0;
+          for (int p = 0; p < PM; ++p) cf[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
+          double v = 0.0;
 #pragma unroll
-        for (int p = PM - 1; p >= 0; --p)
-          if (p < P) v = (p == P - 1) ? cf[p] : fma(v, tv, cf[p]);
-        return v;
-      };
-      bool singular = false;
-      for (int s = 0; s < 64; ++s) {
-        const int i = BWD ? 63 - s : s;
-        double p0 = 0.0, p1 = 0.0;
-        if (!BWD) {
-          int k = t4;
-          for (; k + 4 < i; k += 8) {
-            p0 = fma(horner(k * TILE_LD + i), x[k * S], p0);
-            p1 = fma(horner((k + 4) * TILE_LD + i), x[(k + 4) * S], p1);
+          for (int p = PM - 1; p >= 0; --p)
+            if (p < P) v = (p == P - 1) ? cf[p] : fma(v, tv, cf[p]);
+          return v;
+        };
+        bool singular = false;
+#pragma unroll 1
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const int i = r0 + (BWD ? 15 - s2 : s2);
+          double part = 0.0;
+          if (!BWD) {
+            for (int k = r0 + t4; k < i; k += 4) part = fma(horner(k * TILE_LD + i), x[k * S], part);
+          } else {
+            for (int k = r0 + t4; k < r0 + 16; k += 4)
+              if (k > i) part = fma(horner(i * TILE_LD + k), x[k * S], part);
           }
-          if (k < i) p0 = fma(horner(k * TILE_LD + i), x[k * S], p0);
-        } else {
-          int k = i + 1 + ((t4 - (i + 1)) & 3);  // first k > i with k = t4 mod 4
-          for (; k + 4 < 64; k += 8) {
-            p0 = fma(horner(i * TILE_LD + k), x[k * S], p0);
-            p1 = fma(horner(i * TILE_LD + k + 4), x[(k + 4) * S], p1);
-          }
-          if (k < 64) p0 = fma(horner(i * TILE_LD + k), x[k * S], p0);
+          part += __shfl_xor_sync(0xffffffffu, part, 1);
+          part += __shfl_xor_sync(0xffffffffu, part, 2);
+          const double lii = horner(i * TILE_LD + i);
+          if (!BWD && rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
+          const double xi = (x[i * S] - part) / lii;
+          __syncwarp();
+          if (t4 == 0 && live) x[i * S] = xi;
+          __syncwarp();
         }
-        double part = p0 + p1;
-        part += __shfl_xor_sync(0xffffffffu, part, 1);
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        const double lii = horner(i * TILE_LD + i);
-        if (!BWD && rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
-        const double xi = (x[i * S] - part) / lii;
-        __syncwarp();
-        if (t4 == 0 && live) x[i * S] = xi;
-        __syncwarp();
+        if (!BWD && singular && live && t4 == 0 && (c % m) == 0) singular_any = true;
+        if (!BWD && singular && live && t4 == 0 && (c % m) == 0) a.flags[fold * a.q + l0 + l] = 1;
       }
-      if (!BWD && singular && live && t4 == 0 && (c % m) == 0) a.flags[fold * a.q + l0 + l] = 1;
+      __syncthreads();
+      // rows still to solve: after the block (fwd) / before it (bwd)
+      if (q < 3 && (BWD ? (rg < sb) : (rg > sb))) {
+#pragma unroll
+        for (int i = 0; i < LH; ++i)
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+#pragma unroll
+            for (int j = 0; j < NTA; ++j) acc[i][mt][j][0] = acc[i][mt][j][1] = 0.0;
+#pragma unroll
+            for (int c = 0; c < REMA; ++c) accx[i][mt][c] = 0.0;
+          }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int k = r0 + ks * 4 + t;
+          double th[2][PM];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int row = rg * 16 + mt * 8 + g;
+            // fwd: L(row, k) (column k of the tile); bwd: L(k, row) (column row)
+            const int off = BWD ? row * TILE_LD + k : k * TILE_LD + row;
+#pragma unroll
+            for (int p = 0; p < PM; ++p)
+              if (p < P) th[mt][p] = sD[p * TILE_PLANE + off];
+          }
+          const double* wrow = sR + k * S;
+#pragma unroll
+          for (int i = 0; i < LH; ++i) {
+            const int l = lg * LH + i;
+            if (l < nl) {
+              double b[NTA];
+#pragma unroll
+              for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
+              double rv[REMA];
+#pragma unroll
+              for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) {
+                double av = 0.0;
+#pragma unroll
+                for (int p = PM - 1; p >= 0; --p)
+                  if (p < P) av = (p == P - 1) ? th[mt][p] : fma(av, tl[i], th[mt][p]);
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
+#pragma unroll
+                for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+              }
+            }
+          }
+        }
+        // subtract from this warp's rows (each element owned by exactly one lane)
+#pragma unroll
+        for (int i = 0; i < LH; ++i) {
+          const int l = lg * LH + i;
+          if (l < nl) {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              const int row = rg * 16 + mt * 8 + g;
+#pragma unroll
+              for (int c = 0; c < REM; ++c) {
+                double v = accx[i][mt][c];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                if (t == 0) sR[row * S + l * m + NT * 8 + c] -= v;
+              }
+#pragma unroll
+              for (int j = 0; j < NT; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) sR[row * S + l * m + j * 8 + 2 * t + h] -= acc[i][mt][j][h];
+            }
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
+    (void)singular_any;
     // publish row I: private rows (read back by later slabs through the async proxy) and, for
     // the backward pass, the caller's row-major W (overlapping chunks write identical values)
     for (int i = warp; i < 64; i += NTH / 32) {
