@@ -73,23 +73,35 @@ __global__ void __launch_bounds__(PD_THREADS, 1) potrf_diag_dmma_kernel(double* 
     }
     if (warp == 0) {  // 1b: 16 x 16 factor + inverse
       double* D = a + b0 * PD_LDA + b0;  // D(r, c) = D[c * LDA + r]
+      // register-resident 16 x 16 factor: lane i (< 16) holds row i; column j of L is
+      // broadcast with shuffles (dpotf2 order: sqrt pivot, scale by the reciprocal, rank-1 update)
+      const int ri = lane & 15;
+      double row[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) row[c] = (c <= ri) ? D[c * PD_LDA + ri] : 0.0;
+      int bad = 0;
+#pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const double ajj = D[j * PD_LDA + j];
-        if (!(ajj > 0.0)) {
-          if (lane == 0) fail = k0 + b0 + j + 1;
-          break;
-        }
+        double ajj = __shfl_sync(0xffffffffu, row[j], j);
+        if (!bad && !(ajj > 0.0)) bad = j + 1;  // uniform across the warp
+        if (bad) ajj = 1.0;                       // keep the (discarded) arithmetic finite
         const double ljj = sqrt(ajj), rl = 1.0 / ljj;
-        if (lane > j && lane < 16) D[j * PD_LDA + lane] *= rl;
-        __syncwarp();
-        for (int e = lane; e < 256; e += 32) {
-          const int i = e >> 4, c = e & 15;
-          if (c > j && i >= c) D[c * PD_LDA + i] -= D[j * PD_LDA + i] * D[j * PD_LDA + c];
+        if (ri > j) row[j] *= rl;
+        if (ri == j) row[j] = ljj;
+#pragma unroll
+        for (int c = j + 1; c < 16; ++c) {
+          const double lcj = __shfl_sync(0xffffffffu, row[j], c);  // L(c, j)
+          if (ri >= c) row[c] = fma(-row[j], lcj, row[c]);
         }
-        __syncwarp();
-        if (lane == 0) D[j * PD_LDA + j] = ljj;
-        __syncwarp();
       }
+      if (bad) {
+        if (lane == 0) fail = k0 + b0 + bad;
+      } else if (lane < 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c <= ri) D[c * PD_LDA + ri] = row[c];
+      }
+      __syncwarp();
       if (fail == 0 && lane < 16) {  // column `lane` of D^-1: solve D x = e_c
         const int c = lane;
         double x[16];
