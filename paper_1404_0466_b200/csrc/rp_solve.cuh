@@ -58,7 +58,7 @@ RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 // Warp layout: 8 warps = 4 row groups (16 rows = 2 DMMA m-tiles each) x 2 lambda groups, so
 // every W fragment loaded from shared memory feeds two DMMAs and every coefficient fragment
 // is evaluated for half of the chunk's lambdas.
-template <int NT, int REM, int PT, int LCT, int LG, bool BWD>
+template <int NT, int REM, int PT, int LCT, int LG, int STG, bool BWD>
 __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   constexpr int NTH = 128 * LG;  // 4 row groups x LG lambda groups of warps
   constexpr int LC = LCT ? LCT : SOLVE_LC_GENERIC;
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   const int stageT = P * FWD_SLAB;  // both directions: [k][68] slabs (bwd from the transposed copy)
   const int stageW = 16 * S;
   double* sT = smem;
-  double* sW = smem + SOLVE_STAGES * stageT;
-  const int ring = SOLVE_STAGES * (stageT + stageW);
+  double* sW = smem + STG * stageT;
+  const int ring = STG * (stageT + stageW);
   double* sR = smem + (ring > P * TILE_PLANE ? ring : P * TILE_PLANE);
   uint64_t* full = reinterpret_cast<uint64_t*>(sR + 64 * S);  // per stage, + [3] diagonal tile
 
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   const int cw = nl * m;  // valid chunk columns
   const int64_t wcol0 = (int64_t)l0 * m;
   if (tid == 0) {
-    for (int i = 0; i <= SOLVE_STAGES; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i <= STG; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     // plane slices + the 16 already solved rows of this CTA's private W, completion on full[st]
     auto issue = [&](int s) {
       if (tid == 0 && s < nslab && !(a.dbg & 1)) {
-        const int st = (it0 + s) % SOLVE_STAGES;
+        const int st = (it0 + s) % STG;
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
         const int kq = s & 3;
         const double* tile = thslab + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
@@ -140,13 +140,17 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 
     issue(0);
     issue(1);
-    for (int s = 0; s < nslab; ++s) {
-      // one barrier per slab: after it every warp has finished slab s-1, so its stage can be
-      // refilled with slab s+2; then wait for slab s's bytes
+    // STG == 3: one barrier per slab (refill the stage of slab s-1 with s+2);
+    // STG == 4: one barrier per pair of slabs (refill the stages of s-2, s-1 with s+2, s+3)
+    constexpr int STEP = (STG == 4) ? 2 : 1;
+    for (int s0 = 0; s0 < nslab; s0 += STEP) {
       __syncthreads();
-      issue(s + 2);
-      const int st = (it0 + s) % SOLVE_STAGES;
-      if (!(a.dbg & 1)) mbar_wait(&full[st], ((it0 + s) / SOLVE_STAGES) & 1);
+      issue(s0 + 2);
+      if (STEP == 2) issue(s0 + 3);
+#pragma unroll 1
+    for (int s = s0; s < s0 + STEP; ++s) {
+      const int st = (it0 + s) % STG;
+      if (!(a.dbg & 1)) mbar_wait(&full[st], ((it0 + s) / STG) & 1);
       const double* T = sT + st * stageT;
       const double* Wb = sW + st * stageW;
 #pragma unroll
@@ -196,6 +200,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
     }
+    }
     it0 += nslab;
     __syncthreads();  // every warp is done with the ring
 
@@ -204,8 +209,8 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     double* sD = smem;  // union with the ring (idle during the diagonal step)
     if (tid == 0) {
       const double* tile = theta + (int64_t)tile_index(I, I) * P * TILE_PLANE;
-      mbar_arrive_expect_tx(&full[SOLVE_STAGES], (uint32_t)(P * TILE_PLANE * 8));
-      bulk_g2s(sD, tile, (uint32_t)(P * TILE_PLANE * 8), &full[SOLVE_STAGES]);
+      mbar_arrive_expect_tx(&full[STG], (uint32_t)(P * TILE_PLANE * 8));
+      bulk_g2s(sD, tile, (uint32_t)(P * TILE_PLANE * 8), &full[STG]);
     }
     const int rowI = I * 64;
 #pragma unroll
@@ -244,7 +249,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
     }
-    mbar_wait(&full[SOLVE_STAGES], step & 1);
+    mbar_wait(&full[STG], step & 1);
     __syncthreads();
     // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows: each 16 x 16 diagonal
     // block is solved with 4 lanes per (lambda, output) column (k = t4 mod 4 split, two shuffles);
@@ -392,19 +397,19 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 // bank-conflict free.
 inline int solve_stride(int lam, int m) { return ((lam * m + 3) / 16) * 16 + 12; }
 
-inline size_t solve_smem_bytes(int lam, int m, int P) {
+inline size_t solve_smem_bytes(int lam, int m, int P, int stages = SOLVE_STAGES) {
   const int S = solve_stride(lam, m);
   size_t per_stage = (size_t)P * FWD_SLAB + 16 * (size_t)S;
-  size_t ring = SOLVE_STAGES * per_stage;
+  size_t ring = stages * per_stage;
   size_t diag = (size_t)P * TILE_PLANE;  // theta_II staged into the idle ring during the diagonal step
   return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 8);  // + mbarriers
 }
 
 
-template <int NT, int REM, int PT, int LCT, int LG = 2>
+template <int NT, int REM, int PT, int LCT, int LG = 2, int STG = SOLVE_STAGES>
 int launch_solve(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
-  auto kf = eval_solve_kernel<NT, REM, PT, LCT, LG, false>;
-  auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, true>;
+  auto kf = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, false>;
+  auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, true>;
   cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   kf<<<grid, 128 * LG, smem, st>>>(a);

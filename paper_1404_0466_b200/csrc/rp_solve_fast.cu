@@ -45,8 +45,15 @@ static int ws_pass(const SolveArgs& a, int grid, cudaStream_t st, size_t maxsmem
 template <int M, int P, int LC>
 static int launch_fast(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
   if (!g_solve_ws) {
-    // 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4
-    return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG>(a, grid, smem, st);
+    // 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4.
+    // A 4-stage ring (two slabs per barrier) when it fits in shared memory.
+    int dev = 0, maxsm = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const size_t sm4 = solve_smem_bytes(LC, M, P, 4);
+    if (sm4 <= (size_t)maxsm && !getenv("RP_SOLVE_STG3"))
+      return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, sm4, st);
+    return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, smem, st);
   }
   int dev = 0, maxsmem = 227 * 1024;
   cudaGetDevice(&dev);
