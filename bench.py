@@ -220,7 +220,7 @@ def config_dict(cfg, world):
     return {"workload": f"{cfg.name}: piCholesky {cfg.k}-fold CV sweep", "n": cfg.n, "d": cfg.d, "outputs": cfg.m,
             "folds": cfg.k, "sampled_lambdas": cfg.s, "degree": cfg.r, "grid": cfg.q,
             "lambda_range": [cfg.lo, cfg.hi], "parallelism": f"fold-sharded x{world}",
-            "l2": "inputs (X 3.3 GB at c4) exceed the 126 MB L2; no flush"}
+            "l2": f"inputs (X {cfg.n * cfg.d * 8 / 1e9:.2f} GB) exceed the 126 MB L2; no flush"}
 
 
 # ---------------------------------------------------------------- GPU arm
