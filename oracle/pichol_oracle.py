@@ -300,3 +300,24 @@ def grid_search_pichol(X, Y, assignments, k, grid, g=4, r=2, metric=RMSE,
         out["mean"] = mean
         out["best"] = best
     return out
+
+
+def grid_search_exact(X, Y, assignments, k, grid, metric=RMSE):
+    """cvsearch.py:178-203: one exact factorization per fold per grid point
+    (linalg.cholesky of H + lam I, solve_chol, holdout_error). Returns dict(curves (k, q, m),
+    mean (q, m), best (m,))."""
+    X = np.asarray(X, dtype=float)
+    Y = np.asarray(Y, dtype=float)
+    if Y.ndim == 1:
+        Y = Y[:, None]
+    grid = np.asarray(grid, dtype=float)
+    curves = np.empty((k, grid.shape[0], Y.shape[1]))
+    for i in range(k):
+        val = assignments == i
+        H, G = assemble(X[~val], Y[~val])
+        eye = np.eye(H.shape[0])
+        for j, lam in enumerate(grid):
+            B = solve_chol(cholesky(H + lam * eye), G)
+            curves[i, j] = holdout_error(B, X[val], Y[val], metric)
+    mean, best = merge(curves)
+    return dict(curves=curves, mean=mean, best=best)

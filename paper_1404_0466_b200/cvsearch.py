@@ -350,6 +350,25 @@ def grid_search_pichol(
     return _merge("pichol", grid.values, curves, per_fold, time.perf_counter() - t_start)
 
 
+def grid_search_exact(p, grid, folds, metric=RMSE, threads=None, holdout="auto"):
+    """One exact factorization per fold per grid point, on the device (cvsearch.py:178-203).
+
+    The paper's Chol baseline: H_f + lam I is factored for every lam (batches of 32 per
+    rp_potrf_batched call) and solved with the same fused substitution kernel, q = 1."""
+    from . import exact
+
+    if metric not in METRICS:
+        raise UsageError(f"unknown metric {metric!r}")
+    threads = resolve_threads(threads)
+    t_start = time.perf_counter()
+    X, Y, counts = prepare_design(p, folds)
+    curves = exact.exact_curves(X, Y, counts, grid.values, metric=metric, holdout=holdout)
+    wall = time.perf_counter() - t_start
+    per_fold = _zero_timings()
+    per_fold["factorize"] = wall / folds.k
+    return _merge("chol", grid.values, curves, per_fold, wall)
+
+
 def _fit_basis_checked(sample_lams, r, raw_monomials):
     from .errors import DegenerateSamples, InsufficientSamples
 

@@ -34,6 +34,20 @@ def test_c1_full_sweep_matches_reference():
     assert grid[out["best"][0]] == g["best_lambda"][0]
 
 
+def test_exact_search_matches_reference():  # cvsearch.grid_search_exact, cvsearch.py:178-203
+    g = golden("c1_cv")
+    c1 = configs.CONFIGS["c1"]
+    X, Y = configs.generate(c1)
+    grid = orc.make_grid(c1.lo, c1.hi, c1.q)
+    out = orc.grid_search_exact(X, Y[:, 0], orc.contiguous_assignments(c1.n, c1.k), c1.k, grid)
+    assert np.max(np.abs(out["mean"] - g["exact_mean"]) / g["exact_mean"]) <= 1e-12
+    g = golden("small_multi_cv")
+    grid = orc.make_grid(float(g["lo"]), float(g["hi"]), int(g["q"]))
+    n, k = g["X"].shape[0], int(g["k"])
+    out = orc.grid_search_exact(g["X"], g["Y"], orc.contiguous_assignments(n, k), k, grid)
+    assert np.max(np.abs(out["mean"] - g["exact_mean"]) / g["exact_mean"]) <= 1e-12
+
+
 @pytest.mark.parametrize("name", ["small_multi_cv", "small_misclass_cv"])
 def test_small_cv_matches_reference(name):
     g = golden(name)
