@@ -304,7 +304,7 @@ def run_ours(args, cfg, world, rank, local):
     stage_t = st
 
     # ---- end to end through the public API (pinned host in, curves + argmin out)
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(2, min(args.steps, 3))
+    e2e_steps = max(1, args.e2e_steps) if args.e2e_steps is not None else max(2, min(args.steps, 3))
     sess.run(Xp, Yp)
     barrier()
     t0 = time.perf_counter()

@@ -482,6 +482,88 @@ __global__ void select_kernel(const double* curves, int k, int q, int m, double*
   }
 }
 
+// C_b = X_b^T Y_b for few outputs (m <= 16): a streaming FP64 kernel that reads X once. It is
+// sized to co-reside with the Gram SYRK (128 threads, <= 120 registers next to the SYRK's
+// 288 x 168) and is launched on a side stream, so it runs in the SYRK's shadow: the SYRK is
+// bound by the DMMA pipe at ~5% of HBM bandwidth, this kernel by HBM.
+// CTA = 128 columns of one block; 2 row groups of 64 threads, 2 adjacent columns per thread,
+// rows interleaved across the groups; the partials are combined in a fixed order.
+template <int MT>
+__global__ void __maxnreg__(120) xty_kernel(const double* X, int64_t ldx, int64_t rows, int d, const double* Y,
+                                                  int64_t ldy, int mrt, double* C) {
+  constexpr int MM = MT ? MT : 16;
+  constexpr int RG = 2;
+  const int m = MT ? MT : mrt;
+  __shared__ double red[RG - 1][128];
+  const int b = blockIdx.y, tx = threadIdx.x & 63, grp = threadIdx.x >> 6;
+  const int c = blockIdx.x * 128 + 2 * tx;
+  const double* Xb = X + (int64_t)b * rows * ldx;
+  const double* Yb = Y + (int64_t)b * rows * ldy;
+  double a0[MM], a1[MM];
+#pragma unroll
+  for (int o = 0; o < MM; ++o) a0[o] = a1[o] = 0.0;
+  if (c < d) {
+    const bool pair = c + 1 < d;
+#pragma unroll 4
+    for (int64_t r = grp; r < rows; r += RG) {
+      double x0, x1 = 0.0;
+      if (pair) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(Xb + r * ldx + c));
+        x0 = v.x;
+        x1 = v.y;
+      } else {
+        x0 = __ldcs(Xb + r * ldx + c);
+      }
+      const double* yr = Yb + r * ldy;
+#pragma unroll
+      for (int o = 0; o < MM; ++o)
+        if (o < m) {
+          const double y = __ldg(yr + o);
+          a0[o] = fma(x0, y, a0[o]);
+          a1[o] = fma(x1, y, a1[o]);
+        }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < MM; ++o) {
+    if (o >= m) break;
+    if (grp > 0) {
+      red[grp - 1][2 * tx] = a0[o];
+      red[grp - 1][2 * tx + 1] = a1[o];
+    }
+    __syncthreads();
+    if (grp == 0 && c < d) {
+      double s0 = a0[o], s1 = a1[o];
+      for (int g2 = 0; g2 < RG - 1; ++g2) {
+        s0 += red[g2][2 * tx];
+        s1 += red[g2][2 * tx + 1];
+      }
+      C[((int64_t)b * m + o) * d + c] = s0;
+      if (c + 1 < d) C[((int64_t)b * m + o) * d + c + 1] = s1;
+    }
+    __syncthreads();
+  }
+}
+
+static int xty(const double* X, int64_t ldx, int64_t rows, int nblocks, int d, const double* Y, int64_t ldy, int m,
+               double* C, cudaStream_t st) {
+  dim3 grid((d + 127) / 128, nblocks);
+  switch (m) {
+#define RP_XTY(M) \
+  case M: xty_kernel<M><<<grid, 128, 0, st>>>(X, ldx, rows, d, Y, ldy, m, C); break;
+    RP_XTY(1) RP_XTY(2) RP_XTY(4) RP_XTY(8) RP_XTY(10) RP_XTY(16)
+#undef RP_XTY
+    default: xty_kernel<0><<<grid, 128, 0, st>>>(X, ldx, rows, d, Y, ldy, m, C);
+  }
+  RP_LAUNCH_CHECK("gram xty");
+  return RP_OK;
+}
+
+static const bool g_xty_gemm = [] {
+  const char* e = getenv("RP_XTY_GEMM");
+  return e && e[0] == '1';
+}();
+
 }  // namespace rp
 
 using namespace rp;
@@ -518,10 +600,31 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   a.ldc = d;
   a.strideC = (int64_t)d * d;
   a.lower_only = 1;
+  const bool want_c = m > 0 && C != nullptr;
+  if (want_c) RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
+  const bool side = want_c && m <= 16 && aligned16(X) && ldx % 2 == 0 && !g_xty_gemm;
+  static cudaStream_t xs = nullptr;
+  static cudaEvent_t fork = nullptr, join = nullptr;
+  if (side && !xs) {
+    cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+  }
+  if (side) {  // the side stream starts from the same point of `st` as the SYRK
+    cudaError_t e = cudaEventRecord(fork, st);
+    if (e != cudaSuccess) return cuda_status(e, "gram fork");
+    cudaStreamWaitEvent(xs, fork, 0);
+  }
   int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
   if (rc) return rc;
-  if (m > 0 && C != nullptr) {
-    RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
+  if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
+    rc = xty(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, C, xs);
+    if (rc) return rc;
+    cudaEventRecord(join, xs);
+    cudaStreamWaitEvent(st, join, 0);
+    return RP_OK;
+  }
+  if (want_c) {
     GemmArgs b = gemm_args();
     b.M = d;
     b.N = m;
@@ -587,6 +690,17 @@ size_t rp_potrf_workspace_size(int d, int batch) {
   return sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB;
 }
 
+// The batch is factored as up to CHOL_GROUPS independent groups on their own streams, so one
+// group's latency-bound diagonal kernels (one CTA per matrix) and GEMM tails overlap with the
+// other groups' GEMMs. Each matrix sees the same operation sequence whatever the grouping.
+static int CHOL_GROUPS = [] {
+  const char* e = getenv("RP_CHOL_GROUPS");
+  int v = e ? atoi(e) : 4;  // measured at c4: 1 -> 36.7 ms, 2 -> 34.5, 4 -> 33.6, 5 -> 33.5
+  return v >= 1 && v <= 8 ? v : 4;
+}();
+
+static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, cudaStream_t st);
+
 int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, void* work, void* stream) {
   RP_REQUIRE(d >= 1 && batch >= 1 && stride >= (int64_t)d * d, "rp_potrf_batched: bad sizes");
   cudaStream_t st = (cudaStream_t)stream;
@@ -596,6 +710,35 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(potrf_diag_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PD_SMEM);
+  const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
+  if (groups <= 1 || d <= CHOL_NB) return potrf_group(A, d, stride, batch, info, inv, st);
+  static cudaStream_t gs[8] = {};
+  static cudaEvent_t fork = nullptr, join[8] = {};
+  if (!fork) {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    for (int g = 0; g < 8; ++g) {
+      cudaStreamCreateWithFlags(&gs[g], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&join[g], cudaEventDisableTiming);
+    }
+  }
+  e = cudaEventRecord(fork, st);
+  if (e != cudaSuccess) return cuda_status(e, "potrf fork");
+  int b0 = 0;
+  for (int g = 0; g < groups; ++g) {
+    const int nb = batch / groups + (g < batch % groups ? 1 : 0);
+    cudaStreamWaitEvent(gs[g], fork, 0);
+    int rc = potrf_group(A + (int64_t)b0 * stride, d, stride, nb, info + b0, inv + (int64_t)b0 * CHOL_NB * CHOL_NB,
+                         gs[g]);
+    if (rc) return rc;
+    cudaEventRecord(join[g], gs[g]);
+    cudaStreamWaitEvent(st, join[g], 0);
+    b0 += nb;
+  }
+  return RP_OK;
+}
+
+static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, cudaStream_t st) {
+  const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   // Two-level blocked right-looking factorization. Outer panels of CHOL_OB columns are factored
   // left-looking in 128-column blocks (update from the panel's earlier blocks as one DMMA GEMM,
   // shared-memory diagonal factor + inverse, panel TRSM as a DMMA GEMM against the inverse);

@@ -59,6 +59,21 @@ def test_potrf_batched_and_info(gpu):
         assert np.max(np.abs(L - orc.cholesky(mats[b]))) <= 1e-12 * np.linalg.norm(L)
 
 
+def test_potrf_batched_groups(gpu):
+    # 9 matrices over the stream groups (ragged 3/2/2/2 split), a failure in the second group
+    rng = np.random.default_rng(11)
+    d = 300
+    mats = [make_spd(rng, d) for _ in range(9)]
+    mats[4] = mats[4].copy()
+    mats[4][260, 260] = -1e3
+    dA = _dev.to_dev(np.stack([np.ascontiguousarray(M.T) for M in mats]).reshape(9, -1))
+    info = _ops.potrf(dA, d, 9)
+    assert list(info) == [0, 0, 0, 0, 261, 0, 0, 0, 0]
+    for b in (0, 3, 5, 8):
+        L = np.tril(dA[b].reshape(d, d).cpu().numpy().T)
+        assert np.max(np.abs(L - orc.cholesky(mats[b]))) <= 1e-12 * np.linalg.norm(L)
+
+
 @pytest.mark.parametrize("d,r,s", [(40, 2, 4), (70, 1, 3), (130, 3, 6), (64, 2, 5)])
 def test_fit_tiles_matches_oracle(gpu, d, r, s):
     H = make_spd_spectrum(d, 0.5, 50.0, seed=d)
