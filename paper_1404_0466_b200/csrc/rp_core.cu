@@ -45,13 +45,24 @@ static const bool g_use_ws = [] {
   return !(e && e[0] == '0');
 }();
 
+static const bool g_holdout_full = [] {
+  const char* e = getenv("RP_HOLDOUT_FULL");
+  return e && e[0] == '1';
+}();
+
 // ------------------------------------------------------------------ GEMM dispatch
+
+// Operands the bulk-copy (warp-specialised) GEMM can stream: 16-byte aligned rows and sizes.
+static bool gemm_vec2(const GemmArgs& a, int AL) {
+  return aligned16(a.A) && aligned16(a.B) && a.lda % 2 == 0 && a.ldb % 2 == 0 && a.strideA % 2 == 0 &&
+         a.strideB % 2 == 0 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0);
+}
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
 static int gemm(const GemmArgs& a, int batch, cudaStream_t st, const char* name) {
   if (a.M <= 0 || a.N <= 0 || batch <= 0) return RP_OK;
-  bool vec2 = aligned16(a.A) && aligned16(a.B) && a.lda % 2 == 0 && a.ldb % 2 == 0 && a.strideA % 2 == 0 &&
-              a.strideB % 2 == 0 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0);
+  bool vec2 = gemm_vec2(a, AL);
+  if (a.tri_a && !(vec2 && g_use_ws)) return set_error(RP_EINVAL, "%s: triangular A needs the bulk-copy GEMM", name);
   const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
   if (a.lower_only && (BM != BN || a.M != a.N)) return set_error(RP_EINVAL, "%s: lower_only needs square", name);
   dim3 grid(a.lower_only ? mt * (mt + 1) / 2 : mt * nt, batch);
@@ -416,7 +427,7 @@ __global__ void import_kernel(const double* vec, int d, int P, const int64_t* pe
 
 // sse[f][n] = sum_tm partial[f][tm][n] (fixed order), then curves[f][j][o] from it.
 __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, int m, int64_t n_val, int metric,
-                                      const double* yy, const double* bc, double* curves) {
+                                      const double* yy, const double* bc, double quad_scale, double* curves) {
   const int f = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -425,7 +436,7 @@ __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, 
   double out;
   if (yy) {  // Gram form: n_val * MSE = y^T y - 2 w^T c + w^T G w
     const int o = n % m;
-    double sse = yy[f * m + o] - 2.0 * bc[(int64_t)f * N + n] + s;
+    double sse = yy[f * m + o] - 2.0 * bc[(int64_t)f * N + n] + quad_scale * s;
     out = sqrt((sse > 0.0 ? sse : 0.0) / (double)n_val);
   } else if (metric == RP_METRIC_RMSE) {
     out = sqrt(s / (double)n_val);
@@ -905,7 +916,7 @@ int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows,
   if (rc) return rc;
   const int mtiles = (int)((n_val + 127) / 128);
   holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, metric, nullptr, nullptr,
-                                                             curves);
+                                                             1.0, curves);
   RP_LAUNCH_CHECK("holdout finish");
   return RP_OK;
 }
@@ -934,12 +945,15 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
   a.strideY = w_fold_stride;
   a.ycols = N;
   a.partial = partial;
+  // w^T G w = 2 w^T T w with T = strict_lower(G) + diag(G)/2: half the GEMM, only G's lower
+  // triangle read (RP_HOLDOUT_FULL=1 forces the full product)
+  a.tri_a = (gemm_vec2(a, A_KMAJOR) && g_use_ws && !g_holdout_full) ? 1 : 0;
   int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
   if (rc) return rc;
   holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
   RP_LAUNCH_CHECK("holdout bc");
   holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy, bc,
-                                                             curves);
+                                                             a.tri_a ? 2.0 : 1.0, curves);
   RP_LAUNCH_CHECK("holdout gram finish");
   return RP_OK;
 }

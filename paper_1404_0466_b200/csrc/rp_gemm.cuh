@@ -35,6 +35,10 @@ struct GemmArgs {
   int64_t ldc, strideC;
   double alpha, beta;
   int lower_only;  // square tiles only: compute tiles with tn <= tm (SYRK)
+  // warp-specialised kernel only: A is symmetric and only its lower triangle is used, as
+  // T = strict_lower(A) + diag(A)/2 (so A = T + T^T): row tile tm runs k < (tm+1)*BM, the
+  // diagonal block is masked, and the tiles are walked heaviest first
+  int tri_a;
   // reduction epilogues
   const double* Y;  // EPI_SSE/EPI_MIS: Y(m, o) at Y[m * ldy + o];  EPI_DOTB: B2(m, n) at Y[m*ldy+n]
   int64_t ldy, strideY;
@@ -276,9 +280,17 @@ struct TileCoord {
   int batch, tm, tn;
 };
 
-RP_DEVINL TileCoord ws_tile(const GemmArgs& p, int tile, int mtiles, int ntiles) {
-  const int per = p.lower_only ? mtiles * (mtiles + 1) / 2 : mtiles * ntiles;
+RP_DEVINL TileCoord ws_tile(const GemmArgs& p, int tile, int mtiles, int ntiles, int nbatch) {
   TileCoord c;
+  if (p.tri_a) {  // descending row tile (work ~ tm + 1), then batch, then column tile
+    const int per_tm = ntiles * nbatch;
+    const int rank = tile / per_tm, rem = tile - rank * per_tm;
+    c.tm = mtiles - 1 - rank;
+    c.batch = rem / ntiles;
+    c.tn = rem - c.batch * ntiles;
+    return c;
+  }
+  const int per = p.lower_only ? mtiles * (mtiles + 1) / 2 : mtiles * ntiles;
   c.batch = tile / per;
   int lin = tile - c.batch * per;
   if (p.lower_only) {
@@ -292,6 +304,33 @@ RP_DEVINL TileCoord ws_tile(const GemmArgs& p, int tile, int mtiles, int ntiles)
     c.tn = lin / mtiles;
   }
   return c;
+}
+
+// One 16-deep k-tile of a consumer warp's MT x NT DMMA tile. MASK (triangular A, diagonal block):
+// A(row, k) -> 0 above the diagonal and A/2 on it; rk = (global row - global k) of fragment 0.
+template <int AL, int MT, int NT, int A_STRIDE, int B_STRIDE, bool MASK>
+RP_DEVINL void ws_ktile(double (&acc)[MT][NT][2], const double* a_s, const double* b_s, int arow0, int bcol0, int g,
+                        int t, int rk) {
+#pragma unroll
+  for (int ks = 0; ks < GEMM_BK / 4; ++ks) {
+    const int k = ks * 4 + t;
+    double af[MT], bf[NT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int row = arow0 + i * 8 + g;
+      af[i] = (AL == A_KMAJOR) ? a_s[k * A_STRIDE + row] : a_s[row * A_STRIDE + k];
+      if (MASK) {
+        const int dr = rk + i * 8 + g - k;  // global row - global k
+        af[i] = dr < 0 ? 0.0 : (dr == 0 ? 0.5 * af[i] : af[i]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) bf[j] = b_s[k * B_STRIDE + bcol0 + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
 }
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
@@ -310,7 +349,13 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int mtiles = (p.M + BM - 1) / BM, ntiles = (p.N + BN - 1) / BN;
-  const int ktiles = (p.K + BK - 1) / BK;
+  const int ktiles_all = (p.K + BK - 1) / BK;
+  const int nbatch = total_tiles / (p.lower_only ? mtiles * (mtiles + 1) / 2 : mtiles * ntiles);
+  auto ktiles_of = [&](int tm) {
+    if (EPI != EPI_DOTB || !p.tri_a) return ktiles_all;
+    const int kt = ((tm + 1) * BM + BK - 1) / BK;
+    return kt < ktiles_all ? kt : ktiles_all;
+  };
 
   if (tid == 0) {
     for (int s = 0; s < WS_STAGES; ++s) {
@@ -325,11 +370,12 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
     // ---------------- producer ----------------
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const TileCoord tc = ws_tile(p, tile, mtiles, ntiles);
+      const TileCoord tc = ws_tile(p, tile, mtiles, ntiles, nbatch);
       const int m0 = tc.tm * BM, n0 = tc.tn * BN;
       const int mv = min(BM, p.M - m0), nv = min(BN, p.N - n0);
       const double* A = p.A + tc.batch * p.strideA;
       const double* B = p.B + tc.batch * p.strideB;
+      const int ktiles = ktiles_of(tc.tm);
       for (int kt = 0; kt < ktiles; ++kt, ++it) {
         const int st = it % WS_STAGES;
         mbar_wait(&empty[st], ((it / WS_STAGES) & 1) ^ 1);
@@ -376,9 +422,10 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
   const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   int it = 0;
   for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-    const TileCoord tc = ws_tile(p, tile, mtiles, ntiles);
+    const TileCoord tc = ws_tile(p, tile, mtiles, ntiles, nbatch);
     const int m0 = tc.tm * BM, n0 = tc.tn * BN;
     const int batch = tc.batch;
+    const int ktiles = ktiles_of(tc.tm);
     double acc[MT][NT][2];
 #pragma unroll
     for (int i = 0; i < MT; ++i)
@@ -390,22 +437,11 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
       mbar_wait(&full[st], (it / WS_STAGES) & 1);
       const double* a_s = sA + st * SM::A_ELEMS;
       const double* b_s = sB + st * SM::B_ELEMS;
-#pragma unroll
-      for (int ks = 0; ks < BK / 4; ++ks) {
-        const int k = ks * 4 + t;
-        double af[MT], bf[NT];
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          int row = wm * WM + i * 8 + g;
-          af[i] = (AL == A_KMAJOR) ? a_s[k * SM::A_STRIDE + row] : a_s[row * SM::A_STRIDE + k];
-        }
-#pragma unroll
-        for (int j = 0; j < NT; ++j) bf[j] = b_s[k * SM::B_STRIDE + wn * WN + j * 8 + g];
-#pragma unroll
-        for (int i = 0; i < MT; ++i)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-      }
+      if (EPI == EPI_DOTB && p.tri_a && kt * BK + BK > m0)  // k-tile in the diagonal block: T's mask
+        ws_ktile<AL, MT, NT, SM::A_STRIDE, SM::B_STRIDE, true>(acc, a_s, b_s, wm * WM, wn * WN, g, t,
+                                                              m0 + wm * WM - kt * BK);
+      else
+        ws_ktile<AL, MT, NT, SM::A_STRIDE, SM::B_STRIDE, false>(acc, a_s, b_s, wm * WM, wn * WN, g, t, 0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }

@@ -304,7 +304,8 @@ def sweep_flops(k, n, d, m, q, s, r, nf=None, holdout="gram", n_val=None):
         "solve": nf * q * (2 * r + 4 * m) * D,
     }
     if holdout == "gram":
-        out["holdout"] = nf * 2.0 * d * d * q * m
+        # w^T G_f w from the lower triangle of the symmetric G_f: 2 * D flops per column
+        out["holdout"] = nf * 2.0 * D * q * m
     else:
         out["holdout"] = nf * 2.0 * n_val * d * q * m
     return out
