@@ -75,8 +75,11 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   double* sT = smem;
   double* sW = smem + STG * stageT;
   const int ring = STG * (stageT + stageW);
-  double* sR = smem + (ring > P * TILE_PLANE ? ring : P * TILE_PLANE);
-  uint64_t* full = reinterpret_cast<uint64_t*>(sR + 64 * S);  // per stage, + [3] diagonal tile
+  const int LCr = LCT ? LCT : a.lam_per_cta;
+  const int diagw = P * TILE_PLANE + LCr * (16 * 17 + 16);  // theta_II + evaluated block + pivots
+  double* sR = smem + (ring > diagw ? ring : diagw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sR + 64 * S);  // per stage, + [STG] diagonal tile
+  uint64_t* empty = full + STG + 1;                             // per stage: all warps released it
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -93,6 +96,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   const int64_t wcol0 = (int64_t)l0 * m;
   if (tid == 0) {
     for (int i = 0; i <= STG; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < STG; ++i) mbar_init(&empty[i], NTH / 32);
     fence_mbar_init();
   }
   __syncthreads();
@@ -122,10 +126,13 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       }
 
     // one thread streams slab s: P contiguous 16-column (fwd) / 16-row (bwd, transposed copy)
-    // plane slices + the 16 already solved rows of this CTA's private W, completion on full[st]
+    // plane slices + the 16 already solved rows of this CTA's private W, completion on full[st].
+    // A stage is refilled once every warp has released its previous slab (empty[st]); only the
+    // issuing thread waits for that, the other warps run ahead as far as the data allows.
     auto issue = [&](int s) {
       if (tid == 0 && s < nslab && !(a.dbg & 1)) {
-        const int st = (it0 + s) % STG;
+        const int it = it0 + s, st = it % STG;
+        if (it >= STG) mbar_wait(&empty[st], ((it / STG) + 1) & 1);
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
         const int kq = s & 3;
         const double* tile = thslab + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
@@ -140,15 +147,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 
     issue(0);
     issue(1);
-    // STG == 3: one barrier per slab (refill the stage of slab s-1 with s+2);
-    // STG == 4: one barrier per pair of slabs (refill the stages of s-2, s-1 with s+2, s+3)
-    constexpr int STEP = (STG == 4) ? 2 : 1;
-    for (int s0 = 0; s0 < nslab; s0 += STEP) {
-      __syncthreads();
-      issue(s0 + 2);
-      if (STEP == 2) issue(s0 + 3);
 #pragma unroll 1
-    for (int s = s0; s < s0 + STEP; ++s) {
+    for (int s = 0; s < nslab; ++s) {
+      issue(s + 2);
       const int st = (it0 + s) % STG;
       if (!(a.dbg & 1)) mbar_wait(&full[st], ((it0 + s) / STG) & 1);
       const double* T = sT + st * stageT;
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           }
         }
       }
-    }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
     it0 += nslab;
     __syncthreads();  // every warp is done with the ring
@@ -251,55 +253,61 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     mbar_wait(&full[STG], step & 1);
     __syncthreads();
-    // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows: each 16 x 16 diagonal
-    // block is solved with 4 lanes per (lambda, output) column (k = t4 mod 4 split, two shuffles);
-    // the block's contribution to the remaining rows is then applied with DMMA like a slab
+    // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows. Per 16 x 16 diagonal
+    // block: evaluate it once per lambda into shared memory (with reciprocal pivots and the
+    // singular check), then one thread per (lambda, output) column substitutes with its 16 rows in
+    // registers (column-oriented, so the serial chain is one FMA + one multiply per row); the
+    // block's contribution to the remaining rows of the tile is then applied with DMMA like a slab
     // (A = L(rows, block cols) evaluated from sD, B = the block's solved rows in sR).
-    bool singular_any = false;
+    double* sLev = sD + P * TILE_PLANE;  // [nl][16][17] evaluated block (row i, col j <= i)
+    double* sRinv = sLev + LCr * 16 * 17;  // [nl][16] reciprocal pivots
     for (int q = 0; q < 4; ++q) {
       const int sb = BWD ? 3 - q : q;
       const int r0 = sb * 16;
-      for (int c0 = 0; c0 < ((a.dbg & 2) ? 0 : cw); c0 += NTH / 4) {
-        const int c = c0 + (tid >> 2), t4 = tid & 3;
-        const bool live = c < cw;
-        const int cc = live ? c : cw - 1;
-        const int l = cc / m;
+      for (int e = tid; e < nl * 136; e += NTH) {
+        const int l = e / 136;
+        int ij = e - l * 136;  // packed lower index: row i, col j <= i
+        int i = (int)((sqrt(8.0 * ij + 1.0) - 1.0) * 0.5);
+        while ((i + 1) * (i + 2) / 2 <= ij) ++i;
+        while (i * (i + 1) / 2 > ij) --i;
+        const int j = ij - i * (i + 1) / 2;
         const double tv = a.tvals[l0 + l];
-        const double* th = sD;
-        double* x = sR + cc;
-        // all threads read the same coefficient address at the same time -> smem broadcast
-        auto horner = [&](int off) {
-          double cf[PM];
+        const int off = (r0 + j) * TILE_LD + r0 + i;  // L(r0+i, r0+j), forward (column-major) copy
+        double v = 0.0;
 #pragma unroll
-          for (int p = 0; p < PM; ++p) cf[p] = (p < P) ? th[p * TILE_PLANE + off] : 0.0;
-          double v = 0.0;
-#pragma unroll
-          for (int p = PM - 1; p >= 0; --p)
-            if (p < P) v = (p == P - 1) ? cf[p] : fma(v, tv, cf[p]);
-          return v;
-        };
-        bool singular = false;
-#pragma unroll 1
-        for (int s2 = 0; s2 < 16; ++s2) {
-          const int i = r0 + (BWD ? 15 - s2 : s2);
-          double part = 0.0;
-          if (!BWD) {
-            for (int k = r0 + t4; k < i; k += 4) part = fma(horner(k * TILE_LD + i), x[k * S], part);
-          } else {
-            for (int k = r0 + t4; k < r0 + 16; k += 4)
-              if (k > i) part = fma(horner(i * TILE_LD + k), x[k * S], part);
-          }
-          part += __shfl_xor_sync(0xffffffffu, part, 1);
-          part += __shfl_xor_sync(0xffffffffu, part, 2);
-          const double lii = horner(i * TILE_LD + i);
-          if (!BWD && rowI + i < a.d && !(fabs(lii) >= 1e-12)) singular = true;
-          const double xi = (x[i * S] - part) / lii;
-          __syncwarp();
-          if (t4 == 0 && live) x[i * S] = xi;
-          __syncwarp();
+        for (int p = PM - 1; p >= 0; --p)
+          if (p < P) v = (p == P - 1) ? sD[p * TILE_PLANE + off] : fma(v, tv, sD[p * TILE_PLANE + off]);
+        sLev[(l * 16 + i) * 17 + j] = v;
+        if (i == j) {
+          sRinv[l * 16 + i] = 1.0 / v;
+          if (!BWD && rowI + r0 + i < a.d && !(fabs(v) >= 1e-12)) a.flags[fold * a.q + l0 + l] = 1;
         }
-        if (!BWD && singular && live && t4 == 0 && (c % m) == 0) singular_any = true;
-        if (!BWD && singular && live && t4 == 0 && (c % m) == 0) a.flags[fold * a.q + l0 + l] = 1;
+      }
+      __syncthreads();
+      if (!(a.dbg & 2) && tid < cw) {
+        const int l = tid / m;
+        const double* Lv = sLev + l * 16 * 17;
+        const double* ri = sRinv + l * 16;
+        double x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) x[i] = sR[(r0 + i) * S + tid];
+        if (!BWD) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            x[i] *= ri[i];
+#pragma unroll
+            for (int j = i + 1; j < 16; ++j) x[j] = fma(-Lv[j * 17 + i], x[i], x[j]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 15; i >= 0; --i) {
+            x[i] *= ri[i];
+#pragma unroll
+            for (int j = 0; j < i; ++j) x[j] = fma(-Lv[i * 17 + j], x[i], x[j]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sR[(r0 + i) * S + tid] = x[i];
       }
       __syncthreads();
       // rows still to solve: after the block (fwd) / before it (bwd)
@@ -376,7 +384,6 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       }
       __syncthreads();
     }
-    (void)singular_any;
     // publish row I: private rows (read back by later slabs through the async proxy) and, for
     // the backward pass, the caller's row-major W (overlapping chunks write identical values)
     for (int i = warp; i < 64; i += NTH / 32) {
@@ -401,8 +408,9 @@ inline size_t solve_smem_bytes(int lam, int m, int P, int stages = SOLVE_STAGES)
   const int S = solve_stride(lam, m);
   size_t per_stage = (size_t)P * FWD_SLAB + 16 * (size_t)S;
   size_t ring = stages * per_stage;
-  size_t diag = (size_t)P * TILE_PLANE;  // theta_II staged into the idle ring during the diagonal step
-  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 8);  // + mbarriers
+  // theta_II + the evaluated 16 x 16 diagonal blocks + pivots, in the idle ring during the diagonal step
+  size_t diag = (size_t)P * TILE_PLANE + (size_t)lam * (16 * 17 + 16);
+  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 16);  // + mbarriers
 }
 
 
