@@ -64,11 +64,17 @@ int64_t rp_theta_size(int d, int r);
  * H_f = sum_b G_b - G_f (folds.py contiguous FoldPlan, cvsearch.py:145-147).
  *   X: nblocks * rows_per_block rows, row-major, leading dim ldx (>= d)
  *   Y: same rows, row-major (rows x m), leading dim ldy (>= m); may be NULL when m == 0
- *   G: nblocks x (d x d column-major); only the lower triangle (64-row tiles
- *      at or below the diagonal) is written
- *   C: nblocks x (d x m column-major)  (X_b^T Y_b)                           */
+ *   G: nblocks x (d x d column-major); the lower triangle is written (and the
+ *      upper parts of the tiles that straddle the diagonal)
+ *   C: nblocks x (d x m column-major)  (X_b^T Y_b)
+ *   work: rp_gram_workspace_size(d, rows_per_block, nblocks) bytes (16-byte
+ *      aligned), or NULL. With a workspace and d % 128 == 0, G is computed on
+ *      the int8 tensor cores (tcgen05) by the Ozaki scheme with 8 seven-bit
+ *      slices per value -- FP64-level accuracy (~1e-15 relative to
+ *      sqrt(G_ii G_jj)), NaN/inf propagated; otherwise by FP64 DMMA.   */
+size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks);
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d,
-                   const double* Y, int64_t ldy, int m, double* G, double* C, void* stream);
+                   const double* Y, int64_t ldy, int m, double* G, double* C, void* work, void* stream);
 
 /* Per-block column sums of squares: yy[b][o] = sum_rows Y_b[row][o]^2 (the y^T y term of the
  * Gram-form hold-out error). */

@@ -35,7 +35,8 @@ SIGNATURES = {
     "rp_launch_count": (ctypes.c_longlong, []),
     "rp_tile_count": (_i64, [_i]),
     "rp_theta_size": (_i64, [_i, _i]),
-    "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp]),
+    "rp_gram_workspace_size": (_sz, [_i, _i64, _i]),
+    "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
     "rp_col_sumsq": (_i, [_vp, _i64, _i64, _i, _i, _vp, _vp]),
     "rp_symmetrize": (_i, [_vp, _i, _i64, _i, _vp]),
     "rp_fold_systems": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp]),

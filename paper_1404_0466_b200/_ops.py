@@ -27,7 +27,9 @@ def gram(X, Y=None):
         m, dY = 0, None
     G = _dev.empty((d, d))
     C = _dev.empty((max(m, 1), d))
-    call("rp_gram_blocks", ptr(dX), d, n, 1, d, ptr(dY), max(m, 1), m, ptr(G), ptr(C) if m else None, stream())
+    ws = _dev.workspace(_lib.query("rp_gram_workspace_size", d, n, 1))
+    call("rp_gram_blocks", ptr(dX), d, n, 1, d, ptr(dY), max(m, 1), m, ptr(G), ptr(C) if m else None, ptr(ws),
+         stream())
     call("rp_symmetrize", ptr(G), d, d * d, 1, stream())
     return G, (C[:m] if m else None)
 

@@ -12,6 +12,7 @@
 #include "rp_common.cuh"
 #include "rp_gemm.cuh"
 #include "rp_potrf_diag.cuh"
+#include "rp_ozaki.cuh"
 #include "../../include/ridgepath_b200.h"
 
 namespace rp {
@@ -43,6 +44,11 @@ static const bool g_simple_diag = [] {
 static const bool g_use_ws = [] {
   const char* e = getenv("RP_GEMM_WS");
   return !(e && e[0] == '0');
+}();
+
+static const bool g_gram_dmma = [] {
+  const char* e = getenv("RP_GRAM_DMMA");
+  return e && e[0] == '1';
 }();
 
 static const bool g_holdout_full = [] {
@@ -596,11 +602,20 @@ int64_t rp_tile_count(int d) {
 
 int64_t rp_theta_size(int d, int r) { return 2 * rp_tile_count(d) * (r + 1) * TILE_PLANE; }
 
+size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks) {
+  if (d < 1 || rows_per_block < 1 || nblocks < 1) return 0;
+  return oz_workspace_bytes(OZ_SLICES, d, rows_per_block, nblocks);
+}
+
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d, const double* Y,
-                   int64_t ldy, int m, double* G, double* C, void* stream) {
+                   int64_t ldy, int m, double* G, double* C, void* work, void* stream) {
   RP_REQUIRE(d >= 1 && nblocks >= 1 && rows_per_block >= 1 && ldx >= d, "rp_gram_blocks: bad sizes");
   RP_REQUIRE(rows_per_block <= 0x7fffffff, "rp_gram_blocks: block too tall");
+  RP_REQUIRE(work == nullptr || ((uintptr_t)work & 15) == 0, "rp_gram_blocks: workspace must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
+  // Ozaki-scheme tensor-core Gram (int8 tcgen05) when a workspace is given; RP_GRAM_DMMA=1 forces FP64 DMMA
+  const bool ozaki = work != nullptr && d % OZ_BM == 0 && (int64_t)nblocks * OZ_SLICES * d < 0x7fffffff &&
+                     oz_kpad(rows_per_block) < 0x7fffffff && !g_gram_dmma;
   GemmArgs a = gemm_args();
   a.M = a.N = d;
   a.K = (int)rows_per_block;
@@ -626,7 +641,8 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
     if (e != cudaSuccess) return cuda_status(e, "gram fork");
     cudaStreamWaitEvent(xs, fork, 0);
   }
-  int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
+  int rc = ozaki ? oz_gram<OZ_SLICES>(X, ldx, rows_per_block, nblocks, d, G, work, st)
+                 : gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
   if (rc) return rc;
   if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
     rc = xty(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, C, xs);

@@ -115,6 +115,10 @@ class PicholEngine:
         self.best = torch.empty((m,), dtype=torch.int32, device=dev)
         self.tvals = torch.empty((q,), **f64)
         u8 = dict(dtype=torch.uint8, device=dev)
+        # tensor-core (Ozaki) Gram slices: sized for both call patterns of stage_gram
+        ng = len(self.gram_blocks)
+        self.ws_gram = torch.empty((max(_lib.query("rp_gram_workspace_size", d, self.block_rows[0], ng),
+                                        _lib.query("rp_gram_workspace_size", d, max(self.block_rows), 1)),), **u8)
         self.ws_potrf = torch.empty((_lib.query("rp_potrf_workspace_size", d, nf * s),), **u8)
         self.ws_fit = torch.empty((_lib.query("rp_fit_workspace_size", d, nf),), **u8)
         nval = max(self.block_rows[f] for f in self.local_folds)
@@ -145,7 +149,7 @@ class PicholEngine:
             rows = self.block_rows[0]
             off = int(self.row_off[b0])
             call("rp_gram_blocks", ptr(X[off:]), d, rows, len(blocks), d, ptr(Y[off:]), m, m,
-                 ptr(self.G[b0]), ptr(self.C[b0]), st)
+                 ptr(self.G[b0]), ptr(self.C[b0]), ptr(self.ws_gram), st)
             if self.holdout == "gram":
                 call("rp_col_sumsq", ptr(Y[off:]), m, rows, len(blocks), m, ptr(self.yy[b0]), st)
         else:
@@ -155,7 +159,7 @@ class PicholEngine:
                     cur.wait_event(block_ready[b])
                 off, rows = int(self.row_off[b]), self.block_rows[b]
                 call("rp_gram_blocks", ptr(X[off:]), d, rows, 1, d, ptr(Y[off:]), m, m,
-                     ptr(self.G[b]), ptr(self.C[b]), st)
+                     ptr(self.G[b]), ptr(self.C[b]), ptr(self.ws_gram), st)
                 if self.holdout == "gram":
                     call("rp_col_sumsq", ptr(Y[off:]), m, rows, 1, m, ptr(self.yy[b]), st)
 

@@ -48,9 +48,11 @@ def exact_curves(X, Y, block_rows, grid, metric=RMSE, holdout="auto", batch=MAX_
     G = _dev.empty((k, d, d))
     C = _dev.empty((k, m, d))
     yy = _dev.empty((k, m))
+    ws_gram = _dev.workspace(_lib.query("rp_gram_workspace_size", d, int(max(block_rows)), 1))
     for b in range(k):
         off, rows = int(row_off[b]), int(block_rows[b])
-        call("rp_gram_blocks", ptr(dX[off:]), d, rows, 1, d, ptr(dY[off:]), m, m, ptr(G[b]), ptr(C[b]), st)
+        call("rp_gram_blocks", ptr(dX[off:]), d, rows, 1, d, ptr(dY[off:]), m, m, ptr(G[b]), ptr(C[b]), ptr(ws_gram),
+             st)
         call("rp_col_sumsq", ptr(dY[off:]), m, rows, 1, m, ptr(yy[b]), st)
     B = max(1, min(batch, MAX_BATCH, q))
     Gsum = _dev.empty((d, d))
