@@ -46,7 +46,7 @@ static const bool g_use_ws = [] {
   return !(e && e[0] == '0');
 }();
 
-static const bool g_gram_dmma = [] {
+static bool g_gram_dmma = [] {
   const char* e = getenv("RP_GRAM_DMMA");
   return e && e[0] == '1';
 }();
@@ -604,7 +604,7 @@ int64_t rp_theta_size(int d, int r) { return 2 * rp_tile_count(d) * (r + 1) * TI
 
 size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks) {
   if (d < 1 || rows_per_block < 1 || nblocks < 1) return 0;
-  return oz_workspace_bytes(OZ_SLICES, d, rows_per_block, nblocks);
+  return oz_workspace_bytes(d, rows_per_block, nblocks);
 }
 
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d, const double* Y,
@@ -614,8 +614,7 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   RP_REQUIRE(work == nullptr || ((uintptr_t)work & 15) == 0, "rp_gram_blocks: workspace must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   // Ozaki-scheme tensor-core Gram (int8 tcgen05) when a workspace is given; RP_GRAM_DMMA=1 forces FP64 DMMA
-  const bool ozaki = work != nullptr && d % OZ_BM == 0 && (int64_t)nblocks * OZ_SLICES * d < 0x7fffffff &&
-                     oz_kpad(rows_per_block) < 0x7fffffff && !g_gram_dmma;
+  const bool ozaki = work != nullptr && !g_gram_dmma && oz_supported(d, rows_per_block, nblocks);
   GemmArgs a = gemm_args();
   a.M = a.N = d;
   a.K = (int)rows_per_block;
@@ -641,7 +640,9 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
     if (e != cudaSuccess) return cuda_status(e, "gram fork");
     cudaStreamWaitEvent(xs, fork, 0);
   }
-  int rc = ozaki ? oz_gram<OZ_SLICES>(X, ldx, rows_per_block, nblocks, d, G, work, st)
+  // X_b row-major (rows x d) is the column-major d x rows matrix A_b with lda = ldx: G_b = A_b A_b^T
+  const OzIn oin{X, ldx, rows_per_block * ldx, rows_per_block, d, nblocks};
+  int rc = ozaki ? oz_syrk(oin, G, d, (int64_t)d * d, false, work, st)
                  : gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
   if (rc) return rc;
   if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
@@ -712,11 +713,6 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
   return RP_OK;
 }
 
-size_t rp_potrf_workspace_size(int d, int batch) {
-  (void)d;
-  return sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB;
-}
-
 // The batch is factored as up to CHOL_GROUPS independent groups on their own streams, so one
 // group's latency-bound diagonal kernels (one CTA per matrix) and GEMM tails overlap with the
 // other groups' GEMMs. Each matrix sees the same operation sequence whatever the grouping.
@@ -726,7 +722,45 @@ static int CHOL_GROUPS = [] {
   return v >= 1 && v <= 8 ? v : 4;
 }();
 
-static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, cudaStream_t st);
+// Trailing updates on the int8 tensor cores (Ozaki) instead of FP64 DMMA: off by default. At
+// K = 1024 the two-pass tensor-core tile spends too long in its non-overlapped FP64 epilogue
+// (measured at c4: factorize 37.9 ms DMMA vs 45.1 ms Ozaki); rp_set_option("chol_ozaki", 1) or
+// RP_CHOL_OZAKI=1 enables it.
+static bool g_chol_ozaki = [] {
+  const char* e = getenv("RP_CHOL_OZAKI");
+  return e && e[0] == '1';
+}();
+
+// Per-group slice workspace of the tensor-core trailing update (largest update: d - OB rows).
+static size_t potrf_oz_group_bytes(int d, int batch) {
+  const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
+  const int per = (batch + groups - 1) / groups;
+  const int rem = d - CHOL_OB;
+  if (rem <= 0 || !oz_supported(rem, CHOL_OB, per)) return 0;
+  return (oz_workspace_bytes(rem, CHOL_OB, per) + 1023) / 1024 * 1024;
+}
+
+size_t rp_potrf_workspace_size(int d, int batch) {
+  const size_t inv = ((sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB) + 1023) / 1024 * 1024;
+  const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
+  return inv + (g_chol_ozaki ? (size_t)groups * potrf_oz_group_bytes(d, batch) : 0);
+}
+
+int rp_set_option(const char* name, int value) {
+  RP_REQUIRE(name != nullptr, "rp_set_option: name");
+  if (strcmp(name, "chol_ozaki") == 0) {
+    g_chol_ozaki = value != 0;
+    return RP_OK;
+  }
+  if (strcmp(name, "gram_dmma") == 0) {
+    g_gram_dmma = value != 0;
+    return RP_OK;
+  }
+  return set_error(RP_EINVAL, "rp_set_option: unknown option %s", name);
+}
+
+static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, void* ozws,
+                       cudaStream_t st);
 
 int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, void* work, void* stream) {
   RP_REQUIRE(d >= 1 && batch >= 1 && stride >= (int64_t)d * d, "rp_potrf_batched: bad sizes");
@@ -738,7 +772,11 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(potrf_diag_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PD_SMEM);
   const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
-  if (groups <= 1 || d <= CHOL_NB) return potrf_group(A, d, stride, batch, info, inv, st);
+  // tensor-core trailing updates: one slice workspace per group after inv(L11)
+  const size_t ozg = g_chol_ozaki ? potrf_oz_group_bytes(d, batch) : 0;
+  uint8_t* ozbase = reinterpret_cast<uint8_t*>(work) +
+                    ((sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB) + 1023) / 1024 * 1024;
+  if (groups <= 1 || d <= CHOL_NB) return potrf_group(A, d, stride, batch, info, inv, ozg ? ozbase : nullptr, st);
   static cudaStream_t gs[8] = {};
   static cudaEvent_t fork = nullptr, join[8] = {};
   if (!fork) {
@@ -755,7 +793,7 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
     const int nb = batch / groups + (g < batch % groups ? 1 : 0);
     cudaStreamWaitEvent(gs[g], fork, 0);
     int rc = potrf_group(A + (int64_t)b0 * stride, d, stride, nb, info + b0, inv + (int64_t)b0 * CHOL_NB * CHOL_NB,
-                         gs[g]);
+                         ozg ? ozbase + g * ozg : nullptr, gs[g]);
     if (rc) return rc;
     cudaEventRecord(join[g], gs[g]);
     cudaStreamWaitEvent(st, join[g], 0);
@@ -764,7 +802,8 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   return RP_OK;
 }
 
-static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, cudaStream_t st) {
+static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, void* ozws,
+                       cudaStream_t st) {
   const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   // Two-level blocked right-looking factorization. Outer panels of CHOL_OB columns are factored
   // left-looking in 128-column blocks (update from the panel's earlier blocks as one DMMA GEMM,
@@ -823,6 +862,12 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
     if (rem <= 0) break;
     // A22 -= L21 L21^T with K = ob (lower tiles)
     const double* L21 = A + (int64_t)k0 * d + k0 + ob;
+    if (ozws && oz_supported(rem, ob, batch)) {  // on the int8 tensor cores (Ozaki scheme)
+      const OzIn oin{L21, d, stride, ob, rem, batch};
+      int rc = oz_syrk(oin, A + (int64_t)(k0 + ob) * d + k0 + ob, d, stride, true, ozws, st);
+      if (rc) return rc;
+      continue;
+    }
     GemmArgs u = gemm_args();
     u.M = u.N = rem;
     u.K = ob;

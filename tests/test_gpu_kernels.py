@@ -59,6 +59,32 @@ def test_potrf_batched_and_info(gpu):
         assert np.max(np.abs(L - orc.cholesky(mats[b]))) <= 1e-12 * np.linalg.norm(L)
 
 
+@pytest.fixture
+def chol_ozaki():
+    _lib.call("rp_set_option", b"chol_ozaki", 1)
+    yield
+    _lib.call("rp_set_option", b"chol_ozaki", 0)
+
+
+@pytest.mark.parametrize("d", [1280, 1300, 2176])
+@pytest.mark.parametrize("tensor", [False, True])
+def test_potrf_trailing_update_paths(gpu, request, d, tensor):
+    # d > 1024 runs trailing updates: FP64 DMMA by default; with the option, on the int8 tensor
+    # cores (Ozaki) when (d - 1024) % 128 == 0 (1280, 2176) and DMMA otherwise (1300)
+    if tensor:
+        request.getfixturevalue("chol_ozaki")
+    mats = [make_spd_spectrum(d, 1e-3, 1e2, seed=d + b) for b in range(2)]
+    mats = [0.5 * (M + M.T) for M in mats]
+    dA = _dev.to_dev(np.stack([np.ascontiguousarray(M.T) for M in mats]).reshape(2, -1))
+    info = _ops.potrf(dA, d, 2)
+    assert list(info) == [0, 0]
+    for b in range(2):
+        L = np.tril(dA[b].reshape(d, d).cpu().numpy().T)
+        L_ref = orc.cholesky(mats[b])
+        assert np.linalg.norm(L - L_ref) <= 1e-12 * np.linalg.norm(L_ref)
+        assert np.linalg.norm(L @ L.T - mats[b]) <= 1e-13 * np.linalg.norm(mats[b])
+
+
 def test_potrf_batched_groups(gpu):
     # 9 matrices over the stream groups (ragged 3/2/2/2 split), a failure in the second group
     rng = np.random.default_rng(11)

@@ -22,7 +22,6 @@ int set_error(int code, const char* fmt, ...) {
 void count_launch() {}
 }  // namespace rp
 
-template <int S>
 static int run(int nblocks, int rows, int d, bool full_check, int reps) {
   const size_t n = (size_t)nblocks * rows;
   std::vector<double> X(n * d);
@@ -32,15 +31,18 @@ static int run(int nblocks, int rows, int d, bool full_check, int reps) {
     for (int j = 0; j < d; ++j) X[r * d + j] = nd(gen) / std::sqrt(1.0 + j);
   double *dX, *dG;
   void* work;
-  const size_t wb = rp::oz_workspace_bytes(S, d, rows, nblocks);
+  const size_t wb = rp::oz_workspace_bytes(d, rows, nblocks);
+  const rp::OzIn in{nullptr, d, (int64_t)rows * d, rows, d, nblocks};
   cudaMalloc(&dX, X.size() * 8);
   cudaMalloc(&dG, (size_t)nblocks * d * d * 8);
   cudaMalloc(&work, wb);
   cudaMemcpy(dX, X.data(), X.size() * 8, cudaMemcpyHostToDevice);
   cudaMemset(dG, 0, (size_t)nblocks * d * d * 8);
-  int rc = rp::oz_gram<S>(dX, d, rows, nblocks, d, dG, work, 0);
+  rp::OzIn oin = in;
+  oin.A = dX;
+  int rc = rp::oz_syrk(oin, dG, d, (int64_t)d * d, false, work, 0);
   cudaError_t e = cudaDeviceSynchronize();
-  printf("S=%d nblocks=%d rows=%d d=%d: rc=%d sync=%s\n", S, nblocks, rows, d, rc, cudaGetErrorString(e));
+  printf("nblocks=%d rows=%d d=%d: rc=%d sync=%s\n", nblocks, rows, d, rc, cudaGetErrorString(e));
   if (rc || e != cudaSuccess) return 1;
   std::vector<double> G((size_t)nblocks * d * d);
   cudaMemcpy(G.data(), dG, G.size() * 8, cudaMemcpyDeviceToHost);
@@ -76,9 +78,9 @@ static int run(int nblocks, int rows, int d, bool full_check, int reps) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    rp::oz_gram<S>(dX, d, rows, nblocks, d, dG, work, 0);
+    rp::oz_syrk(oin, dG, d, (int64_t)d * d, false, work, 0);
     cudaEventRecord(e0);
-    for (int r = 0; r < reps; ++r) rp::oz_gram<S>(dX, d, rows, nblocks, d, dG, work, 0);
+    for (int r = 0; r < reps; ++r) rp::oz_syrk(oin, dG, d, (int64_t)d * d, false, work, 0);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -165,13 +167,9 @@ int main(int argc, char** argv) {
     return 0;
   }
   int rc = 0;
-  rc |= run<7>(2, 1000, 256, true, 0);
-  rc |= run<8>(2, 1000, 256, true, 0);
-  rc |= run<7>(1, 40000, 128, true, 0);  // K chunking (kchunk < kpad)
-  if (argc > 1) {
-    rc |= run<7>(8, 12500, 4096, false, 3);
-    rc |= run<8>(8, 12500, 4096, false, 3);
-  }
+  rc |= run(2, 1000, 256, true, 0);
+  rc |= run(1, 40000, 128, true, 0);  // K chunking (kchunk < kpad)
+  if (argc > 1) rc |= run(8, 12500, 4096, false, 3);
   printf("rc=%d\n", rc);
   return rc;
 }
