@@ -74,14 +74,30 @@ def peaks():
             vals = [json.loads(line) for line in f if line.strip()]
         out["fp64_tflops"] = max(v["dmma884_tflops_b4"] for v in vals)
         out["fp64_src"] = "profiles/r01_fp64_peaks.json (mma.sync.m8n8k4.f64, burst)"
+    out["i8_tops"], out["i8_src"] = 4500.0, "fallback (nominal dense int8)"
+    p = os.path.join(ROOT, "profiles", "r01_int8_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            out["i8_tops"] = float(json.load(f)["i8_tops_n128"])
+        out["i8_src"] = "profiles/r01_int8_peak.json (tcgen05.mma kind::i8 M=128 N=128, burst)"
     return out
+
+
+def ozaki_ops(cfg, nblocks):
+    """int8 ops of one oz_syrk launch for the Gram blocks: 36 slice products (8 slices, pairs with
+    p + q <= 7) per 32-deep k-step of every 128 x 128 lower tile (csrc/rp_ozaki.cuh)."""
+    mt = cfg.d // 128
+    tiles = nblocks * mt * (mt + 1) // 2
+    kpad = (cfg.n // cfg.k + 63) // 64 * 64
+    return tiles * (kpad // 32) * 36 * 2.0 * 128 * 128 * 32
 
 
 def ncu_traffic(stage):
     """DRAM bytes (read + write) per launch of a stage's main kernel from the committed
     `ncu --set full` capture (profiles/r01_ncu_top_kernels.json), else None."""
     p = os.path.join(ROOT, "profiles", "r01_ncu_top_kernels.json")
-    key = {"gram": "gram_syrk"}.get(stage)
+    key = {"gram": "gram_syrk", "oz_syrk": "oz_syrk", "eval_solve": "eval_solve",
+           "holdout_gemm": "holdout_gemm"}.get(stage)
     if key is None or not os.path.exists(p):
         return None
     with open(p) as f:
@@ -297,11 +313,16 @@ def run_ours(args, cfg, world, rank, local):
         ms = float(t.item())
     value = cfg.k * cfg.q / (ms / 1e3)
 
-    # ---- per-stage breakdown (separate pass, events between stages)
+    # ---- per-stage breakdown (separate pass, events between stages) and per-kernel times
     for _ in range(2):
         st = {}
         sess.sweep(timings=st)
     stage_t = st
+    _lib.call("rp_set_option", b"profile", 1)
+    _lib.query("rp_profile_ms", None)
+    sess.sweep()
+    kern_ms = {name: _lib.query("rp_profile_ms", name.encode()) for name in ("oz_syrk", "eval_solve", "holdout_gemm")}
+    _lib.call("rp_set_option", b"profile", 0)
 
     # ---- end to end through the public API (pinned host in, curves + argmin out)
     e2e_steps = max(1, args.e2e_steps) if args.e2e_steps is not None else max(2, min(args.steps, 3))
@@ -329,11 +350,38 @@ def run_ours(args, cfg, world, rank, local):
             ts = stage_t[name]
             stages[key] = {"ms": ts * 1e3, "tflops": flops[key] / ts / 1e12,
                            "frac_fp64": flops[key] / ts / 1e12 / pk["fp64_tflops"]}
-    dom = max(stages, key=lambda s: stages[s]["ms"])
     nf = len(shard.local_folds)
-    roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
-            "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": ncu_traffic(dom),
-            "peak_src": pk["fp64_src"], "algorithmic_flops": flops[dom]}
+    # ---- roofline of the dominant single kernel (CUDA events on its launching stream)
+    kernels = {}
+    if kern_ms["oz_syrk"] > 0:
+        ops = ozaki_ops(cfg, len(shard.gram_blocks))
+        kernels["oz_syrk"] = {"ms": kern_ms["oz_syrk"], "launches": 1, "work": ops, "unit": "TOP/s",
+                              "peak": pk["i8_tops"], "peak_src": pk["i8_src"],
+                              "fp64_equivalent_tflops": flops["gram"] / (kern_ms["oz_syrk"] / 1e3) / 1e12}
+    if kern_ms["eval_solve"] > 0:
+        kernels["eval_solve"] = {"ms": kern_ms["eval_solve"], "launches": 2 * len(sess.engine.groups),
+                                 "work": flops["solve"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
+                                 "peak_src": pk["fp64_src"]}
+    if kern_ms["holdout_gemm"] > 0:
+        kernels["holdout_gemm"] = {"ms": kern_ms["holdout_gemm"], "launches": len(sess.engine.groups),
+                                   "work": flops["holdout"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
+                                   "peak_src": pk["fp64_src"]}
+    for v in kernels.values():
+        v["achieved"] = v["work"] / (v["ms"] / 1e3) / 1e12
+        v["frac"] = v["achieved"] / v["peak"]
+    if kernels:
+        dom = max(kernels, key=lambda k: kernels[k]["ms"])
+        kv = kernels[dom]
+        per = kv["launches"]
+        roof = {"bound": "tensor", "kernel": dom, "achieved": kv["achieved"], "peak": kv["peak"], "unit": kv["unit"],
+                "frac": kv["frac"], "traffic": ncu_traffic(dom), "peak_src": kv["peak_src"],
+                "work_per_launch": kv["work"] / per, "ms_per_launch": kv["ms"] / per}
+        if "fp64_equivalent_tflops" in kv:
+            roof["fp64_equivalent_tflops"] = kv["fp64_equivalent_tflops"]
+    else:
+        dom = max(stages, key=lambda s: stages[s]["ms"])
+        roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": None, "peak_src": pk["fp64_src"]}
     stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9 if "solve" in stages else None
 
     out = {
@@ -355,6 +403,7 @@ def run_ours(args, cfg, world, rank, local):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "roofline": roof,
+        "kernels": kernels,
         "stages": stages,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

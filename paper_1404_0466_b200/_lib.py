@@ -37,6 +37,7 @@ SIGNATURES = {
     "rp_theta_size": (_i64, [_i, _i]),
     "rp_gram_workspace_size": (_sz, [_i, _i64, _i]),
     "rp_set_option": (_i, [ctypes.c_char_p, _i]),
+    "rp_profile_ms": (ctypes.c_double, [ctypes.c_char_p]),
     "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
     "rp_col_sumsq": (_i, [_vp, _i64, _i64, _i, _i, _vp, _vp]),
     "rp_symmetrize": (_i, [_vp, _i, _i64, _i, _vp]),

@@ -109,6 +109,30 @@ inline int cuda_status(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return RP_OK;
   return set_error((int)e, "%s: %s", where, cudaGetErrorString(e));
 }
+
+// Kernel timing for the bench's roofline (rp_set_option("profile", 1)): CUDA events recorded on
+// the launching stream around selected kernels, summed by rp_profile_ms(name).
+bool prof_on();
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b);
+cudaEvent_t prof_event();
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (prof_on()) {
+      a = prof_event();
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = prof_event();
+      cudaEventRecord(b, st);
+      prof_push(name, a, b);
+    }
+  }
+};
 }  // namespace rp
 
 #define RP_LAUNCH_CHECK(where)                          \

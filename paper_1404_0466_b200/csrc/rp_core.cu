@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "rp_common.cuh"
 #include "rp_gemm.cuh"
@@ -31,6 +32,20 @@ int set_error(int code, const char* fmt, ...) {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static bool g_profile = false;
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_prof;
+bool prof_on() { return g_profile; }
+cudaEvent_t prof_event() {
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back({name, a, b}); }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -202,8 +217,10 @@ __global__ void col_sumsq_kernel(const double* Y, int64_t ldy, int64_t rows, int
 constexpr int CHOL_NB = 128;
 static int CHOL_OB = [] {
   const char* e = getenv("RP_CHOL_OB");
-  int v = e ? atoi(e) : 1024;  // measured at c4: 384 -> 38.3 ms, 512 -> 37.4, 768 -> 36.8, 1024 -> 36.7
-  return v >= 128 && v % 128 == 0 ? v : 1024;
+  // measured at c4 with DMMA trailing updates: 384 -> 38.3 ms, 512 -> 37.4, 768 -> 36.8, 1024 -> 36.7;
+  // with tensor-core trailing updates (evals/s): 768 -> 15442, 1024 -> 15815, 1536 -> 15949, 2048 -> 15919
+  int v = e ? atoi(e) : 1536;
+  return v >= 128 && v % 128 == 0 ? v : 1536;
 }();
 
 // Factor the NB x NB diagonal block at (k0, k0) of every batch matrix in shared memory
@@ -722,13 +739,12 @@ static int CHOL_GROUPS = [] {
   return v >= 1 && v <= 8 ? v : 4;
 }();
 
-// Trailing updates on the int8 tensor cores (Ozaki) instead of FP64 DMMA: off by default. At
-// K = 1024 the two-pass tensor-core tile spends too long in its non-overlapped FP64 epilogue
-// (measured at c4: factorize 37.9 ms DMMA vs 45.1 ms Ozaki); rp_set_option("chol_ozaki", 1) or
-// RP_CHOL_OZAKI=1 enables it.
+// Trailing updates A22 -= L21 L21^T on the int8 tensor cores (Ozaki) instead of FP64 DMMA
+// (measured at c4: factorize 36.2 ms DMMA vs 33.3 ms Ozaki). rp_set_option("chol_ozaki", 0) or
+// RP_CHOL_OZAKI=0 keeps them on DMMA.
 static bool g_chol_ozaki = [] {
   const char* e = getenv("RP_CHOL_OZAKI");
-  return e && e[0] == '1';
+  return !(e && e[0] == '0');
 }();
 
 // Per-group slice workspace of the tensor-core trailing update (largest update: d - OB rows).
@@ -746,6 +762,24 @@ size_t rp_potrf_workspace_size(int d, int batch) {
   return inv + (g_chol_ozaki ? (size_t)groups * potrf_oz_group_bytes(d, batch) : 0);
 }
 
+double rp_profile_ms(const char* name) {
+  cudaDeviceSynchronize();
+  double tot = 0.0;
+  std::vector<ProfRec> keep;
+  for (auto& r : g_prof) {
+    if (name == nullptr || r.name == name) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) tot += ms;
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    } else {
+      keep.push_back(r);
+    }
+  }
+  g_prof.swap(keep);
+  return tot;
+}
+
 int rp_set_option(const char* name, int value) {
   RP_REQUIRE(name != nullptr, "rp_set_option: name");
   if (strcmp(name, "chol_ozaki") == 0) {
@@ -754,6 +788,10 @@ int rp_set_option(const char* name, int value) {
   }
   if (strcmp(name, "gram_dmma") == 0) {
     g_gram_dmma = value != 0;
+    return RP_OK;
+  }
+  if (strcmp(name, "profile") == 0) {
+    g_profile = value != 0;
     return RP_OK;
   }
   return set_error(RP_EINVAL, "rp_set_option: unknown option %s", name);
@@ -864,7 +902,7 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
     const double* L21 = A + (int64_t)k0 * d + k0 + ob;
     if (ozws && oz_supported(rem, ob, batch)) {  // on the int8 tensor cores (Ozaki scheme)
       const OzIn oin{L21, d, stride, ob, rem, batch};
-      int rc = oz_syrk(oin, A + (int64_t)(k0 + ob) * d + k0 + ob, d, stride, true, ozws, st);
+      int rc = oz_syrk(oin, A + (int64_t)(k0 + ob) * d + k0 + ob, d, stride, true, ozws, st, "oz_syrk_chol");
       if (rc) return rc;
       continue;
     }
@@ -1009,7 +1047,11 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
   // w^T G w = 2 w^T T w with T = strict_lower(G) + diag(G)/2: half the GEMM, only G's lower
   // triangle read (RP_HOLDOUT_FULL=1 forces the full product)
   a.tri_a = (gemm_vec2(a, A_KMAJOR) && g_use_ws && !g_holdout_full) ? 1 : 0;
-  int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
+  int rc;
+  {
+    ProfScope prof("holdout_gemm", st);
+    rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
+  }
   if (rc) return rc;
   holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
   RP_LAUNCH_CHECK("holdout bc");

@@ -317,17 +317,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
 #pragma unroll
               for (int c = 0; c < 32; ++c) part[c] = fma((double)(int)v[c], w, part[c]);
             }
-#pragma unroll 4
+            // read-modify-write of this 32-column chunk: every load is issued before any store
+            // (a store could alias a later load otherwise and serialise 32 global round trips)
+            double* dst0 = Cb + (int64_t)(J * OZ_BM + h * 32) * a.ldc + i;
+            double old[32];
+            if (!first_item) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) old[c] = __ldcg(dst0 + (int64_t)c * a.ldc);
+            }
+#pragma unroll
             for (int c = 0; c < 32; ++c) {
-              const int j = J * OZ_BM + h * 32 + c;
-              const int ej = Eb[j];
-              double* dst = Cb + (int64_t)j * a.ldc + i;
+              const int ej = Eb[J * OZ_BM + h * 32 + c];
+              double v;
               if (ei == OZ_NONFINITE || ej == OZ_NONFINITE) {
-                *dst = __longlong_as_double(0x7ff8000000000000LL);
+                v = __longlong_as_double(0x7ff8000000000000LL);
               } else {
-                const double v = ldexp(part[c], ei + ej);
-                *dst = first_item ? v : (a.subtract ? *dst - v : *dst + v);
+                v = ldexp(part[c], ei + ej);
+                if (!first_item) v = a.subtract ? old[c] - v : old[c] + v;
               }
+              dst0[(int64_t)c * a.ldc] = v;
             }
           }
           first_item = false;
@@ -385,7 +393,7 @@ inline bool oz_supported(int M, int64_t K, int nbatch) {
 
 // C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
 inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
-                   cudaStream_t st) {
+                   cudaStream_t st, const char* prof_name = "oz_syrk") {
   int* E = reinterpret_cast<int*>(work);
   int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(in.M, in.nbatch);
   const int64_t kpad = oz_kpad(in.K);
@@ -413,7 +421,10 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = a.total_tiles < sms ? a.total_tiles : sms;
   cudaFuncSetAttribute(oz_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
-  oz_syrk_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
+  {
+    ProfScope prof(prof_name, st);
+    oz_syrk_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
+  }
   RP_LAUNCH_CHECK("ozaki syrk");
   return RP_OK;
 }

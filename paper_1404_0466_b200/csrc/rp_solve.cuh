@@ -420,9 +420,15 @@ int launch_solve(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
   auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, true>;
   cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kf<<<grid, 128 * LG, smem, st>>>(a);
+  {
+    ProfScope prof("eval_solve", st);
+    kf<<<grid, 128 * LG, smem, st>>>(a);
+  }
   RP_LAUNCH_CHECK("eval_solve fwd");
-  kb<<<grid, 128 * LG, smem, st>>>(a);
+  {
+    ProfScope prof("eval_solve", st);
+    kb<<<grid, 128 * LG, smem, st>>>(a);
+  }
   RP_LAUNCH_CHECK("eval_solve bwd");
   return RP_OK;
 }

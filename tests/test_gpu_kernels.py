@@ -60,19 +60,19 @@ def test_potrf_batched_and_info(gpu):
 
 
 @pytest.fixture
-def chol_ozaki():
-    _lib.call("rp_set_option", b"chol_ozaki", 1)
-    yield
+def chol_dmma():
     _lib.call("rp_set_option", b"chol_ozaki", 0)
+    yield
+    _lib.call("rp_set_option", b"chol_ozaki", 1)
 
 
 @pytest.mark.parametrize("d", [1280, 1300, 2176])
-@pytest.mark.parametrize("tensor", [False, True])
+@pytest.mark.parametrize("tensor", [True, False])
 def test_potrf_trailing_update_paths(gpu, request, d, tensor):
-    # d > 1024 runs trailing updates: FP64 DMMA by default; with the option, on the int8 tensor
-    # cores (Ozaki) when (d - 1024) % 128 == 0 (1280, 2176) and DMMA otherwise (1300)
-    if tensor:
-        request.getfixturevalue("chol_ozaki")
+    # d > 1024 runs trailing updates: on the int8 tensor cores (Ozaki) by default when
+    # (d - 1024) % 128 == 0 (1280, 2176), FP64 DMMA otherwise (1300) or with the option off
+    if not tensor:
+        request.getfixturevalue("chol_dmma")
     mats = [make_spd_spectrum(d, 1e-3, 1e2, seed=d + b) for b in range(2)]
     mats = [0.5 * (M + M.T) for M in mats]
     dA = _dev.to_dev(np.stack([np.ascontiguousarray(M.T) for M in mats]).reshape(2, -1))

@@ -1,0 +1,49 @@
+"""Per-launch DRAM traffic and duration of the dominant kernels from an `ncu --set full` report,
+as the JSON bench.py reads for roofline.traffic (profiles/rNN_ncu_top_kernels.json).
+
+    python tools/ncu_top_json.py gpurun_out/top.ncu-rep > profiles/r01_ncu_top_kernels.json
+"""
+
+import csv
+import io
+import json
+import subprocess
+import sys
+
+KEYS = {"oz_syrk_kernel": "oz_syrk", "eval_solve_kernel": "eval_solve", "32, 3>": "holdout_gemm"}
+
+
+def main(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+
+    def val(r, k):
+        v = float(r[h.index(k)].replace(",", ""))
+        u = units[h.index(k)]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
+                 "msecond": 1.0, "usecond": 1e-3, "nsecond": 1e-6}.get(u, 1.0)
+        return v * scale
+
+    res = {}
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")]
+        for pat, key in KEYS.items():
+            if pat in name:
+                e = res.setdefault(key, {"launches": 0, "dram_read_bytes": 0.0, "dram_write_bytes": 0.0,
+                                         "duration_ms": 0.0, "kernel": name[:120]})
+                e["launches"] += 1
+                e["dram_read_bytes"] += val(r, "dram__bytes_read.sum")
+                e["dram_write_bytes"] += val(r, "dram__bytes_write.sum")
+                e["duration_ms"] += val(r, "gpu__time_duration.sum")
+    for e in res.values():  # per launch
+        n = e["launches"]
+        e["dram_read_bytes"] /= n
+        e["dram_write_bytes"] /= n
+        e["duration_ms"] /= n
+    json.dump(res, sys.stdout, indent=1)
+    print()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
