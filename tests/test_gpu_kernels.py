@@ -180,3 +180,60 @@ def test_engine_sweep_matches_oracle(gpu, holdout, n, d, m, k, q, s, r):
     assert rel(curves.cpu().numpy(), ref["curves"]) <= 1e-8
     assert rel(mean.cpu().numpy(), ref["mean"]) <= 1e-8
     assert np.array_equal(best.cpu().numpy(), ref["best"])
+
+
+# ---------------------------------------------------------------- tensor-core (Ozaki) Gram
+
+
+def normalized_err(G, G_ref):
+    s = np.sqrt(np.outer(np.diag(G_ref), np.diag(G_ref)))
+    s[s == 0] = 1.0
+    return np.max(np.abs(np.tril(G) - np.tril(G_ref)) / s)
+
+
+@pytest.mark.parametrize("n,d", [(1000, 256), (40000, 128), (3000, 384)])
+def test_ozaki_gram_fp64_level(gpu, n, d):
+    # per-column scales over 200 orders of magnitude; 40000 rows cut K into int32-safe chunks
+    rng = np.random.default_rng(n + d)
+    X = rng.standard_normal((n, d)) * np.logspace(-50, 50, d)
+    G, _ = _ops.gram(X, None)
+    G = _dev.colmajor_to_host(G.reshape(-1), d)
+    G_ref = X.T @ X
+    assert normalized_err(G, G_ref) <= 1e-14
+
+
+@pytest.fixture
+def gram_dmma():
+    _lib.call("rp_set_option", b"gram_dmma", 1)
+    yield
+    _lib.call("rp_set_option", b"gram_dmma", 0)
+
+
+def test_ozaki_gram_matches_dmma_gram(gpu, request):
+    X, Y = configs.powerlaw(2500, 512, 3, seed=5)
+    G1, C1 = _ops.gram(X, Y)
+    request.getfixturevalue("gram_dmma")
+    G2, C2 = _ops.gram(X, Y)
+    G1 = _dev.colmajor_to_host(G1.reshape(-1), 512)
+    G2 = _dev.colmajor_to_host(G2.reshape(-1), 512)
+    err = normalized_err(G1, G2)
+    assert err <= 5e-15, err
+    assert np.array_equal(C1.cpu().numpy(), C2.cpu().numpy())  # X^T Y takes the same path
+
+
+def test_ozaki_gram_zero_and_nonfinite_columns(gpu):
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal((700, 256))
+    X[:, 5] = 0.0
+    X[123, 17] = np.nan
+    X[9, 200] = np.inf
+    G, _ = _ops.gram(X, None)
+    G = _dev.colmajor_to_host(G.reshape(-1), 256)
+    bad = np.zeros(256, bool)
+    bad[[17, 200]] = True
+    mask = bad[:, None] | bad[None, :]
+    assert np.all(np.isnan(G[mask]))
+    assert np.all(G[5, ~bad] == 0.0) and np.all(G[~bad, 5] == 0.0)
+    keep = ~mask
+    G_ref = np.nan_to_num(X).T @ np.nan_to_num(X)
+    assert normalized_err(np.where(keep, G, 0.0), np.where(keep, G_ref, 0.0)) <= 1e-14
