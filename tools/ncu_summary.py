@@ -17,6 +17,11 @@ KEYS = [
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA pipe %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "DFMA pipe %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe (tcgen05) active %"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput %"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit rate %"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput %"),
     ("dram__bytes_read.sum", "DRAM read"),
     ("dram__bytes_write.sum", "DRAM write"),
     ("launch__registers_per_thread", "registers"),
