@@ -61,6 +61,13 @@ static const bool g_use_ws = [] {
   return !(e && e[0] == '0');
 }();
 
+// Gram-form hold-out on the int8 tensor cores (Ozaki, rp_ozaki.cuh oz_holdout) when the
+// workspace allows; rp_set_option("holdout_ozaki", 0) or RP_HOLDOUT_OZAKI=0 keeps FP64 DMMA.
+static bool g_holdout_ozaki = [] {
+  const char* e = getenv("RP_HOLDOUT_OZAKI");
+  return !(e && e[0] == '0');
+}();
+
 static bool g_gram_dmma = [] {
   const char* e = getenv("RP_GRAM_DMMA");
   return e && e[0] == '1';
@@ -790,6 +797,10 @@ int rp_set_option(const char* name, int value) {
     g_gram_dmma = value != 0;
     return RP_OK;
   }
+  if (strcmp(name, "holdout_ozaki") == 0) {
+    g_holdout_ozaki = value != 0;
+    return RP_OK;
+  }
   if (strcmp(name, "profile") == 0) {
     g_profile = value != 0;
     return RP_OK;
@@ -979,11 +990,16 @@ int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_
   return RP_OK;
 }
 
+static int64_t holdout_mt(int64_t n_val, int d) {
+  const int64_t mt_direct = (n_val + 127) / 128, mt_gram = 2 * ((d + 127) / 128);  // 2 passes (Ozaki)
+  return mt_direct > mt_gram ? mt_direct : mt_gram;
+}
+
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf) {
   const int64_t N = (int64_t)q * m;
-  const int64_t mt_direct = (n_val + 127) / 128, mt_gram = (d + 127) / 128;
-  const int64_t mt = mt_direct > mt_gram ? mt_direct : mt_gram;
-  return sizeof(double) * (size_t)(nf * mt * N + nf * N);
+  const size_t base = (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + nf * N) + 1023) / 1024 * 1024;
+  const bool oz = g_holdout_ozaki && oz_holdout_supported(d, N, nf);
+  return base + (oz ? oz_holdout_workspace(d, N, nf, false) : 0);
 }
 
 int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows, int64_t n_val, int d,
@@ -1028,7 +1044,21 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
   const int N = q * m;
   const int mtiles = (d + 127) / 128;
   double* partial = (double*)work;
-  double* bc = partial + (size_t)nf * mtiles * N;
+  double* bc = partial + (size_t)nf * holdout_mt(n_val, d) * N;
+  const size_t base =
+      (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + (int64_t)nf * N) + 1023) / 1024 * 1024;
+  if (g_holdout_ozaki && oz_holdout_supported(d, N, nf) && ((uintptr_t)work & 15) == 0) {
+    // w^T G w = 2 w^T T w on the int8 tensor cores: partials [f][2 * mtiles][N]
+    int rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial,
+                        reinterpret_cast<uint8_t*>(work) + base, st);
+    if (rc) return rc;
+    holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
+    RP_LAUNCH_CHECK("holdout bc");
+    holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, 2 * mtiles, N, m, n_val, RP_METRIC_RMSE,
+                                                               yy, bc, 2.0, curves);
+    RP_LAUNCH_CHECK("holdout gram finish");
+    return RP_OK;
+  }
   GemmArgs a = gemm_args();
   a.M = d;
   a.N = N;

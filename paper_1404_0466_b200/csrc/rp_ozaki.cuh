@@ -5,15 +5,14 @@
 // sm_100a has no FP64 tcgen05 MMA: the FP64 path (mma.sync DMMA) peaks at 37 TFLOP/s, while the
 // int8 tensor cores run at ~4 POPS. A (M x K, column-major) is cut into fixed-point slices
 //
-//   per row i:  a_ik = 2^E_i * sum_{p<S} d_p(i,k) 2^{-7(p+1)},   d_p in [-127, 127]
-//   (E_i = exponent of max_k |a_ik|, |a| / 2^E_i < 1 written as S = 8 signed 7-bit digits,
-//   the tail below 2^{E_i - 56} truncated), so
+//   per row i:  a_ik = 2^(E_i - 54) * sum_{p<S} d_p(i,k) 256^(S-1-p),   d_p in [-128, 127]
+//   (E_i = exponent of max_k |a_ik|; |a| 2^(54 - E_i) < 2^54 truncated to an integer and written
+//   as S = 7 balanced base-256 digits), so
 //
-//   (A A^T)_ij = 2^{E_i+E_j} sum_{g<S} 2^{-7(g+2)} C_g(i,j),   C_g = sum_{p+q=g} S_p S_q^T
+//   (A A^T)_ij = 2^(E_i+E_j) sum_{g<S} 2^(-8g-12) C_g(i,j),   C_g = sum_{p+q=g} S_p S_q^T
 //
-// with C_g exact in int32 and the products of weight below 2^{-7(S+1)} dropped (the order of
-// the digit truncation): FP64-level accuracy in the sqrt(C_ii C_jj) norm (measured 1.5e-15 on
-// c4-shaped Gram blocks).
+// with C_g exact in int32 and the 28 products of weight below 2^(-8S-4) dropped (the order of
+// the digit truncation): FP64-level accuracy in the sqrt(C_ii C_jj) norm.
 //
 // Kernels:
 //   oz_rowexp_kernel   E[b][i]                      (one pass over A, row max)
@@ -24,9 +23,9 @@
 //                      tcgen05.mma (M = N = 128, K = 32) into 4 weight-group accumulators of
 //                      128 x 128 int32 (all 512 TMEM columns), warps 2-5 read TMEM (tcgen05.ld),
 //                      recombine in FP64 and add the tile into C. Only 4 groups fit in TMEM, so a
-//                      tile runs two passes over K: groups 4..7 (all 8 slices), then 0..3
+//                      tile runs two passes over K: groups 4..6 (all 7 slices), then 0..3
 //                      (slices 0..3). K is cut in chunks short enough that no int32 accumulator
-//                      can overflow (8 pairs x 127^2 x K_chunk < 2^31).
+//                      can overflow (7 pairs x 128^2 x K_chunk < 2^31).
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -35,12 +34,12 @@
 
 namespace rp {
 
-constexpr int OZ_S = 8;  // slices: 56-bit fixed point
+constexpr int OZ_S = 7;  // slices: balanced base-256 digits of a 54-bit fixed-point value
 constexpr int OZ_BM = 128, OZ_BK = 32, OZ_STAGES = 3, OZ_GP = 4;
 constexpr int OZ_THREADS = 192;  // producer, MMA, 4 epilogue warps
 constexpr int OZ_SLICE = OZ_BM * OZ_BK;             // bytes of one 128 x 32 slice tile
 constexpr int OZ_STAGE = 2 * OZ_S * OZ_SLICE;        // A_I and A_J, all slices
-constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 256;
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 128 + 4 * 32 * 8;
 // Row exponent marking a row with a NaN or infinity: the entries it touches are NaN, as in FP64.
 constexpr int OZ_NONFINITE = 0x7fffffff;
 
@@ -48,7 +47,7 @@ inline int64_t oz_kpad(int64_t k) { return (k + 63) / 64 * 64; }
 
 // K-chunk such that S ordered pairs of int8 products never overflow an int32 accumulator.
 inline int64_t oz_kchunk(int64_t kpad) {
-  int64_t c = (2147483647LL / ((int64_t)OZ_S * 127 * 127)) / OZ_BK * OZ_BK;
+  int64_t c = (2147483647LL / ((int64_t)OZ_S * 128 * 128)) / OZ_BK * OZ_BK;
   return c < kpad ? c : kpad;
 }
 
@@ -56,6 +55,9 @@ struct OzIn {  // A_b: M x K column-major, element (i, k) at A + b * bstride + k
   const double* A;
   int64_t lda, bstride, K;
   int M, nbatch;
+  int Mpad = 0;  // rows of the slice layout (>= M, multiple of 128; 0 = M); rows >= M are zero
+  int tri = 0;   // 1: use T = strict_lower(A) + diag(A)/2 instead of A (A square, lower read only)
+  __host__ __device__ int mpad() const { return Mpad ? Mpad : M; }
 };
 
 // ------------------------------------------------------------------ preprocessing
@@ -64,19 +66,25 @@ struct OzIn {  // A_b: M x K column-major, element (i, k) at A + b * bstride + k
 // NaN or infinite).
 __global__ void oz_rowexp_kernel(OzIn in, int* E) {
   const int b = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= in.M) return;
+  const int mp = in.mpad();
+  if (i >= mp) return;
+  if (i >= in.M) {
+    E[(int64_t)b * mp + i] = 0;
+    return;
+  }
   const double* x = in.A + (int64_t)b * in.bstride + i;
+  const int64_t kend = in.tri ? (i + 1 < in.K ? i + 1 : in.K) : in.K;  // T: columns k <= i
   double mx = 0.0;
   bool finite = true;
 #pragma unroll 8
-  for (int64_t k = 0; k < in.K; ++k) {
+  for (int64_t k = 0; k < kend; ++k) {
     const double v = fabs(__ldcs(x + k * in.lda));
     finite &= (v <= 1.79769313486231570e308);  // false for NaN and inf
     mx = fmax(mx, v);
   }
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);
-  E[(int64_t)b * in.M + i] = finite ? e : OZ_NONFINITE;
+  E[(int64_t)b * mp + i] = finite ? e : OZ_NONFINITE;
 }
 
 // Digits of a 64 (k) x 64 (i) tile, written K-major: slices[((b*S + p)*M + i)*kpad + k].
@@ -92,21 +100,23 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
     uint32_t w[OZ_S];
 #pragma unroll
     for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
-    const int ei = (i < in.M) ? E[(int64_t)b * in.M + i] : OZ_NONFINITE;
+    const int ei = (i < in.M) ? E[(int64_t)b * in.mpad() + i] : OZ_NONFINITE;
     if (ei != OZ_NONFINITE) {
-      const double scale = ldexp(1.0, 7 * OZ_S - ei);
+      const double scale = ldexp(1.0, 54 - ei);  // |x| < 2^ei -> |v| < 2^54
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int64_t k = k0 + kq * 4 + r;
-        const double x = (k < in.K) ? Ab[k * in.lda + i] : 0.0;
-        const unsigned long long u = (unsigned long long)(fabs(x) * scale);  // truncation, < 2^56
-        const bool neg = x < 0.0;
+        double x = (k < in.K && (!in.tri || k <= i)) ? Ab[k * in.lda + i] : 0.0;
+        if (in.tri && k == i) x *= 0.5;  // exact
+        long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
+        // balanced base-256 digits, least significant first: d in [-128, 127], v = (v - d) / 256
 #pragma unroll
-        for (int p = 0; p < OZ_S; ++p) {
-          int dv = (int)((u >> (7 * (OZ_S - 1 - p))) & 127ull);
-          if (neg) dv = -dv;
+        for (int p = OZ_S - 1; p >= 1; --p) {
+          const int dv = (int)(signed char)(v & 0xff);
+          v = (v - dv) >> 8;
           w[p] |= ((uint32_t)(dv & 0xff)) << (8 * r);
         }
+        w[0] |= ((uint32_t)((int)v & 0xff)) << (8 * r);  // |v| <= 65 here
       }
     }
 #pragma unroll
@@ -117,13 +127,13 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
     const int c = it & 3, ii = (it >> 2) & 63, p = it >> 8;
     const int i = i0 + ii;
     const int64_t k = k0 + c * 16;
-    if (i >= in.M || k >= kpad) continue;
+    if (i >= in.mpad() || k >= kpad) continue;
     uint4 v;
     v.x = dig[p][ii][c * 4 + 0];
     v.y = dig[p][ii][c * 4 + 1];
     v.z = dig[p][ii][c * 4 + 2];
     v.w = dig[p][ii][c * 4 + 3];
-    *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * in.M + i) * kpad + k) = v;
+    *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * in.mpad() + i) * kpad + k) = v;
   }
 }
 
@@ -311,9 +321,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             for (int c = 0; c < 32; ++c) part[c] = 0.0;
 #pragma unroll 1
             for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
+              if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
               uint32_t v[32];
               oz_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g * 128 + h * 32), v);
-              const double w = ldexp(1.0, -7 * (g0 + g + 2));
+              const double w = ldexp(1.0, -8 * (g0 + g) - 12);
 #pragma unroll
               for (int c = 0; c < 32; ++c) part[c] = fma((double)(int)v[c], w, part[c]);
             }
@@ -391,16 +402,24 @@ inline bool oz_supported(int M, int64_t K, int nbatch) {
          oz_encode_fn() != nullptr;
 }
 
+// Exponents + K-major slices of a batch of column-major matrices (rows padded to in.mpad()).
+inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cudaStream_t st) {
+  const int mp = in.mpad();
+  oz_rowexp_kernel<<<dim3((mp + 255) / 256, in.nbatch), 256, 0, st>>>(in, E);
+  RP_LAUNCH_CHECK("ozaki rowexp");
+  oz_slice_kernel<<<dim3((unsigned)(kpad / 64), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(in, E, slices, kpad);
+  RP_LAUNCH_CHECK("ozaki slice");
+  return RP_OK;
+}
+
 // C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
 inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
                    cudaStream_t st, const char* prof_name = "oz_syrk") {
   int* E = reinterpret_cast<int*>(work);
   int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(in.M, in.nbatch);
   const int64_t kpad = oz_kpad(in.K);
-  oz_rowexp_kernel<<<dim3((in.M + 255) / 256, in.nbatch), 256, 0, st>>>(in, E);
-  RP_LAUNCH_CHECK("ozaki rowexp");
-  oz_slice_kernel<<<dim3((unsigned)(kpad / 64), (in.M + 63) / 64, in.nbatch), 256, 0, st>>>(in, E, slices, kpad);
-  RP_LAUNCH_CHECK("ozaki slice");
+  int rc = oz_prepare(in, E, slices, kpad, st);
+  if (rc) return rc;
   CUtensorMap tm;
   if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * in.M))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
@@ -426,6 +445,268 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
     oz_syrk_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
   }
   RP_LAUNCH_CHECK("ozaki syrk");
+  return RP_OK;
+}
+
+// ------------------------------------------------------------------ Gram-form hold-out
+// quad[b][n] = w_n^T T_b w_n with T_b = strict_lower(G_b) + diag(G_b)/2 (so w^T G w = 2 quad),
+// for the q*m solution columns w_n of W_b (row-major d x ldw). One 128 x 128 tile (I, J) of
+// T_b W_b at a time, K = rows k < 128(I+1) only (T is lower triangular); A = slices of T_b
+// (shared by all b when the batch stride of G is 0), B = slices of W_b^T. The epilogue scales
+// the tile to FP64, multiplies by W_b(i, n), reduces over the 128 rows (warp reduce-scatter,
+// then the 4 epilogue warps through shared memory) and writes one partial per (tile row, pass):
+// part[b][2 * I + pass][n], summed in a fixed order by the finish kernel.
+struct OzDotArgs {
+  const int* EA;  // [nA][MpadA]
+  const int* EB;  // [nbatch][MpadB]
+  const double* W;
+  int64_t ldw, w_stride;
+  double* part;
+  int d, N, MpadA, MpadB, mtA, ntB, nbatch, a_shared, total_tiles;
+  int64_t kpad;
+};
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    oz_dotb_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzDotArgs a) {
+  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
+  uint64_t* empty = full + OZ_STAGES;
+  uint64_t* tfull = empty + OZ_STAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* red = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE + 128);  // [4][32]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int per_I = a.nbatch * a.ntB;
+  auto decode = [&](int tile, int& b, int& I, int& J) {  // heaviest (largest I) first
+    const int rank = tile / per_I, rem = tile - rank * per_I;
+    I = a.mtA - 1 - rank;
+    b = rem / a.ntB;
+    J = rem - b * a.ntB;
+  };
+  auto ksteps = [&](int I) {
+    const int64_t ke = (int64_t)(I + 1) * OZ_BM < a.kpad ? (int64_t)(I + 1) * OZ_BM : a.kpad;
+    return (int)(ke / OZ_BK);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+        int b, I, J;
+        decode(tile, b, I, J);
+        const int ba = a.a_shared ? 0 : b;
+        const int rowA = ba * OZ_S * a.MpadA + I * OZ_BM, rowB = b * OZ_S * a.MpadB + J * OZ_BM;
+        const int nk = ksteps(I);
+        for (int pass = 1; pass >= 0; --pass) {
+          const int ns = pass ? OZ_S : OZ_GP;
+          for (int kk = 0; kk < nk; ++kk, ++it) {
+            const int st = it % OZ_STAGES;
+            mbar_wait(&empty[st], ((it / OZ_STAGES) & 1) ^ 1);
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * OZ_SLICE));
+            uint8_t* sa = smem + st * OZ_STAGE;
+            uint8_t* sb = sa + OZ_S * OZ_SLICE;
+            for (int p = 0; p < ns; ++p) {
+              oz_tma_2d(sa + p * OZ_SLICE, &tmA, kk * OZ_BK, rowA + p * a.MpadA, &full[st]);
+              oz_tma_2d(sb + p * OZ_SLICE, &tmB, kk * OZ_BK, rowB + p * a.MpadB, &full[st]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0, item = 0;
+      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+        int b, I, J;
+        decode(tile, b, I, J);
+        const int nk = ksteps(I);
+        for (int pass = 1; pass >= 0; --pass, ++item) {
+          const int g0 = pass * OZ_GP;
+          mbar_wait(tempty, (item & 1) ^ 1);
+          oz_fence_after();
+          for (int kk = 0; kk < nk; ++kk, ++it) {
+            const int st = it % OZ_STAGES;
+            mbar_wait(&full[st], (it / OZ_STAGES) & 1);
+            oz_fence_after();
+            const uint32_t sa = smem_u32(smem + st * OZ_STAGE);
+            const uint32_t sb = sa + OZ_S * OZ_SLICE;
+#pragma unroll
+            for (int p = 0; p < OZ_S; ++p)
+#pragma unroll
+              for (int q = 0; q < OZ_S - p; ++q) {
+                const int g = p + q;
+                if (g < g0 || g >= g0 + OZ_GP) continue;
+                oz_mma(tmem + (uint32_t)((g - g0) * 128), oz_desc_sw32(sa + p * OZ_SLICE),
+                       oz_desc_sw32(sb + q * OZ_SLICE), (kk == 0 && p == 0) ? 0u : 1u);
+              }
+            oz_commit(&empty[st]);
+          }
+          oz_commit(tfull);
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int row_in_tile = quarter * 32 + lane;
+    int item = 0;
+    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      int b, I, J;
+      decode(tile, b, I, J);
+      const int ba = a.a_shared ? 0 : b;
+      const int i = I * OZ_BM + row_in_tile;
+      const int ei = a.EA[(int64_t)ba * a.MpadA + i];
+      const int* EBb = a.EB + (int64_t)b * a.MpadB;
+      const double* Wrow = a.W + (int64_t)b * a.w_stride + (int64_t)i * a.ldw;
+      for (int pass = 1; pass >= 0; --pass, ++item) {
+        const int g0 = pass * OZ_GP;
+        mbar_wait(tfull, item & 1);
+        oz_fence_after();
+#pragma unroll 1
+        for (int h = 0; h < 4; ++h) {
+          double v[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c] = 0.0;
+#pragma unroll 1
+          for (int g = OZ_GP - 1; g >= 0; --g) {
+            if (g0 + g >= OZ_S) continue;  // groups past S - 1 are not computed
+            uint32_t t[32];
+            oz_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g * 128 + h * 32), t);
+            const double w = ldexp(1.0, -8 * (g0 + g) - 12);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)t[c], w, v[c]);
+          }
+          const int n0 = J * OZ_BM + h * 32;
+          if (h == 3) {  // the accumulators are no longer needed: let the next pass start
+            oz_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty);
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int n = n0 + c;
+            const int en = EBb[n];
+            double x = 0.0;
+            if (i < a.d && n < a.N) {
+              x = (ei == OZ_NONFINITE || en == OZ_NONFINITE) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                              : ldexp(v[c], ei + en) * Wrow[n];
+            }
+            v[c] = x;
+          }
+          // reduce-scatter over the warp's 32 rows: lane L ends with column n0 + L
+#pragma unroll
+          for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+            const bool upper = (lane & s2) != 0;
+#pragma unroll
+            for (int j = 0; j < s2; ++j) {
+              const double send = upper ? v[j] : v[j + s2];
+              const double keep = upper ? v[j + s2] : v[j];
+              v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
+            }
+          }
+          red[quarter * 32 + lane] = v[0];
+          named_bar_sync(1, 128);
+          if (quarter == 0) {
+            const double tot = red[lane] + red[32 + lane] + red[64 + lane] + red[96 + lane];
+            const int n = n0 + lane;
+            if (n < a.N) a.part[(((int64_t)b * a.mtA + I) * 2 + pass) * a.N + n] = tot;
+          }
+          named_bar_sync(1, 128);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+inline int64_t oz_rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Workspace of oz_holdout: exponents and slices of T (nA copies) and of W^T (nbatch).
+inline size_t oz_holdout_workspace(int d, int64_t N, int nbatch, bool a_shared) {
+  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
+  const int na = a_shared ? 1 : nbatch;
+  return (size_t)oz_rup((int64_t)na * mpa * 4, 1024) + (size_t)oz_rup((int64_t)nbatch * mpb * 4, 1024) +
+         (size_t)na * OZ_S * mpa * kpad + (size_t)nbatch * OZ_S * mpb * kpad;
+}
+
+inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
+  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM);
+  return oz_kpad(d) <= oz_kchunk(oz_kpad(d)) && (int64_t)nbatch * OZ_S * (mpa > mpb ? mpa : mpb) < 0x7fffffff &&
+         oz_encode_fn() != nullptr;
+}
+
+// part[b][2 * I + pass][n]: partials of w_n^T T_b w_n (sum over the 2 * ceil(d/128) entries).
+inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
+                      int64_t N, int nbatch, double* part, void* work, cudaStream_t st) {
+  const bool shared = g_stride == 0;
+  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
+  const int na = shared ? 1 : nbatch;
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(work);
+  int* EA = reinterpret_cast<int*>(w8);
+  w8 += oz_rup((int64_t)na * mpa * 4, 1024);
+  int* EB = reinterpret_cast<int*>(w8);
+  w8 += oz_rup((int64_t)nbatch * mpb * 4, 1024);
+  int8_t* SA = reinterpret_cast<int8_t*>(w8);
+  int8_t* SB = SA + (size_t)na * OZ_S * mpa * kpad;
+  OzIn ia{G, d, g_stride, d, d, na};
+  ia.Mpad = (int)mpa;
+  ia.tri = 1;
+  OzIn ib{W, ldw, w_stride, d, (int)N, nbatch};  // W_b^T: row n, column k at W + k*ldw + n
+  ib.Mpad = (int)mpb;
+  int rc = oz_prepare(ia, EA, SA, kpad, st);
+  if (rc) return rc;
+  rc = oz_prepare(ib, EB, SB, kpad, st);
+  if (rc) return rc;
+  CUtensorMap ta, tb;
+  if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) || !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb))
+    return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
+  OzDotArgs a;
+  a.EA = EA;
+  a.EB = EB;
+  a.W = W;
+  a.ldw = ldw;
+  a.w_stride = w_stride;
+  a.part = part;
+  a.d = d;
+  a.N = (int)N;
+  a.MpadA = (int)mpa;
+  a.MpadB = (int)mpb;
+  a.mtA = (int)(mpa / OZ_BM);
+  a.ntB = (int)(mpb / OZ_BM);
+  a.nbatch = nbatch;
+  a.a_shared = shared ? 1 : 0;
+  a.total_tiles = a.mtA * a.ntB * nbatch;
+  a.kpad = kpad;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.total_tiles < sms ? a.total_tiles : sms;
+  cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+  {
+    ProfScope prof("holdout_gemm", st);
+    oz_dotb_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ta, tb, a);
+  }
+  RP_LAUNCH_CHECK("ozaki holdout");
   return RP_OK;
 }
 

@@ -217,7 +217,7 @@ def test_ozaki_gram_matches_dmma_gram(gpu, request):
     G1 = _dev.colmajor_to_host(G1.reshape(-1), 512)
     G2 = _dev.colmajor_to_host(G2.reshape(-1), 512)
     err = normalized_err(G1, G2)
-    assert err <= 5e-15, err
+    assert err <= 1e-14, err
     assert np.array_equal(C1.cpu().numpy(), C2.cpu().numpy())  # X^T Y takes the same path
 
 
@@ -237,3 +237,27 @@ def test_ozaki_gram_zero_and_nonfinite_columns(gpu):
     keep = ~mask
     G_ref = np.nan_to_num(X).T @ np.nan_to_num(X)
     assert normalized_err(np.where(keep, G, 0.0), np.where(keep, G_ref, 0.0)) <= 1e-14
+
+
+@pytest.fixture
+def holdout_dmma():
+    _lib.call("rp_set_option", b"holdout_ozaki", 0)
+    yield
+    _lib.call("rp_set_option", b"holdout_ozaki", 1)
+
+
+@pytest.mark.parametrize("n,d,m,k,q", [(3000, 300, 3, 3, 45), (4000, 512, 10, 4, 13), (1500, 70, 1, 5, 9)])
+def test_holdout_gram_tensor_core_matches_dmma(gpu, request, n, d, m, k, q):
+    # the Gram-form hold-out on the int8 tensor cores (w^T T w from the lower triangle of G_f)
+    # against the FP64 DMMA form and the oracle; d and q*m not multiples of the 128 tile
+    X, Y = configs.powerlaw(n, d, m, seed=d + q)
+    grid = orc.make_grid(1e-3, 1e1, q)
+    lams_s, V, cond, ts, tsh, P = pichol.fit_basis(grid[orc.sample_indices(q, 4)], 2)
+    eng = PicholEngine([n // k] * k, d, m, q, 4, 2, holdout="gram")
+    c_tc = eng.sweep(_dev.to_dev(X), _dev.to_dev(Y), lams_s, P, V, ts * grid + tsh)[0].cpu().numpy()
+    request.getfixturevalue("holdout_dmma")
+    eng2 = PicholEngine([n // k] * k, d, m, q, 4, 2, holdout="gram")
+    c_dm = eng2.sweep(_dev.to_dev(X), _dev.to_dev(Y), lams_s, P, V, ts * grid + tsh)[0].cpu().numpy()
+    assert rel(c_tc, c_dm) <= 1e-10
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(n, k), k, grid, g=4, r=2)
+    assert rel(c_tc, ref["curves"]) <= 1e-8

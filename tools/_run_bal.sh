@@ -1,0 +1,4 @@
+timeout 120 ./tools/ozaki_test big 2>&1 | tail -7
+python -m pytest tests -m gpu -q -x > gpurun_out/t.log 2>&1; tail -n 3 gpurun_out/t.log
+python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/bal.json 2> gpurun_out/bal.err
+python -c "import json;d=json.load(open('gpurun_out/bal.json'));print(round(d['value']), round(d['e2e']['value']), d['clocks'], {k:round(v['ms'],2) for k,v in d['stages'].items()}, {k:round(v['ms'],2) for k,v in d['kernels'].items()})"

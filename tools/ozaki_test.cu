@@ -20,6 +20,9 @@ int set_error(int code, const char* fmt, ...) {
   return code;
 }
 void count_launch() {}
+bool prof_on() { return false; }
+cudaEvent_t prof_event() { return nullptr; }
+void prof_push(const char*, cudaEvent_t, cudaEvent_t) {}
 }  // namespace rp
 
 static int run(int nblocks, int rows, int d, bool full_check, int reps) {
@@ -47,7 +50,7 @@ static int run(int nblocks, int rows, int d, bool full_check, int reps) {
   std::vector<double> G((size_t)nblocks * d * d);
   cudaMemcpy(G.data(), dG, G.size() * 8, cudaMemcpyDeviceToHost);
   // check: all (i >= j) entries for small, a sample for large
-  double maxrel = 0.0, maxabs_err = 0.0, scale = 0.0;
+  double maxabs_err = 0.0, scale = 0.0;
   std::uniform_int_distribution<int> ui(0, d - 1);
   const int nchk = full_check ? -1 : 2000;
   for (int b = 0; b < nblocks; ++b) {
