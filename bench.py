@@ -83,13 +83,26 @@ def peaks():
     return out
 
 
+OZ_PAIRS = 28  # 7 balanced base-256 slices, products with p + q <= 6 (csrc/rp_ozaki.cuh)
+
+
 def ozaki_ops(cfg, nblocks):
-    """int8 ops of one oz_syrk launch for the Gram blocks: 36 slice products (8 slices, pairs with
-    p + q <= 7) per 32-deep k-step of every 128 x 128 lower tile (csrc/rp_ozaki.cuh)."""
+    """int8 ops of one oz_syrk launch for the Gram blocks: 28 slice products per 32-deep k-step
+    of every 128 x 128 lower tile."""
     mt = cfg.d // 128
     tiles = nblocks * mt * (mt + 1) // 2
     kpad = (cfg.n // cfg.k + 63) // 64 * 64
-    return tiles * (kpad // 32) * 36 * 2.0 * 128 * 128 * 32
+    return tiles * (kpad // 32) * OZ_PAIRS * 2.0 * 128 * 128 * 32
+
+
+def ozaki_holdout_ops(cfg, nf, mg):
+    """int8 ops of the tensor-core Gram-form hold-out (w^T T w): row tile I of T runs the k-steps
+    k < 128 (I + 1); columns are the q * m solution vectors (padded to 128)."""
+    mt = (cfg.d + 127) // 128
+    kpad = (cfg.d + 63) // 64 * 64
+    nt = (cfg.q * mg + 127) // 128
+    ksteps = sum(min(128 * (i + 1), kpad) // 32 for i in range(mt))
+    return nf * nt * ksteps * OZ_PAIRS * 2.0 * 128 * 128 * 32
 
 
 def ncu_traffic(stage):
@@ -97,7 +110,7 @@ def ncu_traffic(stage):
     `ncu --set full` capture (profiles/r01_ncu_top_kernels.json), else None."""
     p = os.path.join(ROOT, "profiles", "r01_ncu_top_kernels.json")
     key = {"gram": "gram_syrk", "oz_syrk": "oz_syrk", "eval_solve": "eval_solve",
-           "holdout_gemm": "holdout_gemm"}.get(stage)
+           "holdout_gemm": "holdout_gemm", "oz_holdout": "oz_holdout"}.get(stage)
     if key is None or not os.path.exists(p):
         return None
     with open(p) as f:
@@ -321,7 +334,8 @@ def run_ours(args, cfg, world, rank, local):
     _lib.call("rp_set_option", b"profile", 1)
     _lib.query("rp_profile_ms", None)
     sess.sweep()
-    kern_ms = {name: _lib.query("rp_profile_ms", name.encode()) for name in ("oz_syrk", "eval_solve", "holdout_gemm")}
+    kern_ms = {name: _lib.query("rp_profile_ms", name.encode())
+               for name in ("oz_syrk", "eval_solve", "holdout_gemm", "oz_holdout")}
     _lib.call("rp_set_option", b"profile", 0)
 
     # ---- end to end through the public API (pinned host in, curves + argmin out)
@@ -362,6 +376,11 @@ def run_ours(args, cfg, world, rank, local):
         kernels["eval_solve"] = {"ms": kern_ms["eval_solve"], "launches": 2 * len(sess.engine.groups),
                                  "work": flops["solve"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
                                  "peak_src": pk["fp64_src"]}
+    if kern_ms["oz_holdout"] > 0:
+        ops = sum(ozaki_holdout_ops(cfg, nf, c1 - c0) for c0, c1 in sess.engine.groups)
+        kernels["oz_holdout"] = {"ms": kern_ms["oz_holdout"], "launches": len(sess.engine.groups), "work": ops,
+                                 "unit": "TOP/s", "peak": pk["i8_tops"], "peak_src": pk["i8_src"],
+                                 "fp64_equivalent_tflops": flops["holdout"] / (kern_ms["oz_holdout"] / 1e3) / 1e12}
     if kern_ms["holdout_gemm"] > 0:
         kernels["holdout_gemm"] = {"ms": kern_ms["holdout_gemm"], "launches": len(sess.engine.groups),
                                    "work": flops["holdout"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],

@@ -64,76 +64,98 @@ struct OzIn {  // A_b: M x K column-major, element (i, k) at A + b * bstride + k
 
 // E[b][i]: exponent with max_k |a_ik| < 2^E (0 for an all-zero row, OZ_NONFINITE if any entry is
 // NaN or infinite).
-__global__ void oz_rowexp_kernel(OzIn in, int* E) {
-  const int b = blockIdx.y, i = blockIdx.x * blockDim.x + threadIdx.x;
+// One CTA per 32 rows: 8 warps stride over k (each warp reads 32 contiguous rows of A per k:
+// coalesced), then a max-reduction over the warps in shared memory.
+__global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E) {
+  __shared__ double smx[8][32];
+  __shared__ int sfin[8][32];
+  const int b = blockIdx.y, lane = threadIdx.x & 31, wk = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
   const int mp = in.mpad();
-  if (i >= mp) return;
-  if (i >= in.M) {
-    E[(int64_t)b * mp + i] = 0;
-    return;
-  }
-  const double* x = in.A + (int64_t)b * in.bstride + i;
-  const int64_t kend = in.tri ? (i + 1 < in.K ? i + 1 : in.K) : in.K;  // T: columns k <= i
   double mx = 0.0;
   bool finite = true;
-#pragma unroll 8
-  for (int64_t k = 0; k < kend; ++k) {
-    const double v = fabs(__ldcs(x + k * in.lda));
-    finite &= (v <= 1.79769313486231570e308);  // false for NaN and inf
-    mx = fmax(mx, v);
+  if (i < in.M) {
+    const double* x = in.A + (int64_t)b * in.bstride + i;
+    const int64_t kend = in.tri ? (i + 1 < in.K ? i + 1 : in.K) : in.K;  // T: columns k <= i
+#pragma unroll 4
+    for (int64_t k = wk; k < kend; k += 8) {
+      const double v = fabs(__ldcs(x + k * in.lda));
+      finite &= (v <= 1.79769313486231570e308);  // false for NaN and inf
+      mx = fmax(mx, v);
+    }
   }
-  int e = 0;
-  if (mx > 0.0) frexp(mx, &e);
-  E[(int64_t)b * mp + i] = finite ? e : OZ_NONFINITE;
+  smx[wk][lane] = mx;
+  sfin[wk][lane] = finite ? 1 : 0;
+  __syncthreads();
+  if (wk == 0 && i < mp) {
+    for (int w = 1; w < 8; ++w) {
+      mx = fmax(mx, smx[w][lane]);
+      finite = finite && sfin[w][lane];
+    }
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    E[(int64_t)b * mp + i] = (i < in.M && !finite) ? OZ_NONFINITE : e;
+  }
 }
 
-// Digits of a 64 (k) x 64 (i) tile, written K-major: slices[((b*S + p)*M + i)*kpad + k].
-// Columns past K and rows past M give zero digits.
+// Digits of 64 (i) x 256 (k) of A, in four 64 x 64 sub-tiles, written K-major:
+// slices[((b*S + p)*Mpad + i)*kpad + k]. Columns past K and rows past M give zero digits.
 __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, int8_t* slices, int64_t kpad) {
   __shared__ uint32_t dig[OZ_S][64][17];  // [p][i][k/4], 4 digits per word, padded rows
   const int b = blockIdx.z, i0 = blockIdx.y * 64;
-  const int64_t k0 = (int64_t)blockIdx.x * 64;
   const double* Ab = in.A + (int64_t)b * in.bstride;
-  for (int it = threadIdx.x; it < 64 * 16; it += 256) {
-    const int ii = it & 63, kq = it >> 6;  // consecutive threads: consecutive rows (contiguous)
-    const int i = i0 + ii;
-    uint32_t w[OZ_S];
+  const int mp = in.mpad();
+  for (int sub = 0; sub < 4; ++sub) {
+    const int64_t k0 = (int64_t)blockIdx.x * 256 + sub * 64;
+    if (k0 >= kpad) break;
+    for (int it = threadIdx.x; it < 64 * 16; it += 256) {
+      const int ii = it & 63, kq = it >> 6;  // consecutive threads: consecutive rows (contiguous)
+      const int i = i0 + ii;
+      uint32_t w[OZ_S];
 #pragma unroll
-    for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
-    const int ei = (i < in.M) ? E[(int64_t)b * in.mpad() + i] : OZ_NONFINITE;
-    if (ei != OZ_NONFINITE) {
-      const double scale = ldexp(1.0, 54 - ei);  // |x| < 2^ei -> |v| < 2^54
+      for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
+      const int ei = (i < in.M) ? E[(int64_t)b * mp + i] : OZ_NONFINITE;
+      if (ei != OZ_NONFINITE) {
+        const double scale = ldexp(1.0, 54 - ei);  // |x| < 2^ei -> |v| < 2^54
+        double xs[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int64_t k = k0 + kq * 4 + r;
-        double x = (k < in.K && (!in.tri || k <= i)) ? Ab[k * in.lda + i] : 0.0;
-        if (in.tri && k == i) x *= 0.5;  // exact
-        long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
-        // balanced base-256 digits, least significant first: d in [-128, 127], v = (v - d) / 256
-#pragma unroll
-        for (int p = OZ_S - 1; p >= 1; --p) {
-          const int dv = (int)(signed char)(v & 0xff);
-          v = (v - dv) >> 8;
-          w[p] |= ((uint32_t)(dv & 0xff)) << (8 * r);
+        for (int r = 0; r < 4; ++r) {
+          const int64_t k = k0 + kq * 4 + r;
+          xs[r] = (k < in.K && (!in.tri || k <= i)) ? __ldcs(Ab + k * in.lda + i) : 0.0;
         }
-        w[0] |= ((uint32_t)((int)v & 0xff)) << (8 * r);  // |v| <= 65 here
-      }
-    }
 #pragma unroll
-    for (int p = 0; p < OZ_S; ++p) dig[p][ii][kq] = w[p];
-  }
-  __syncthreads();
-  for (int it = threadIdx.x; it < OZ_S * 64 * 4; it += 256) {
-    const int c = it & 3, ii = (it >> 2) & 63, p = it >> 8;
-    const int i = i0 + ii;
-    const int64_t k = k0 + c * 16;
-    if (i >= in.mpad() || k >= kpad) continue;
-    uint4 v;
-    v.x = dig[p][ii][c * 4 + 0];
-    v.y = dig[p][ii][c * 4 + 1];
-    v.z = dig[p][ii][c * 4 + 2];
-    v.w = dig[p][ii][c * 4 + 3];
-    *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * in.mpad() + i) * kpad + k) = v;
+        for (int r = 0; r < 4; ++r) {
+          const int64_t k = k0 + kq * 4 + r;
+          double x = xs[r];
+          if (in.tri && k == i) x *= 0.5;  // exact
+          long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
+          // balanced base-256 digits, least significant first: d in [-128, 127], v = (v - d) / 256
+#pragma unroll
+          for (int p = OZ_S - 1; p >= 1; --p) {
+            const int dv = (int)(signed char)(v & 0xff);
+            v = (v - dv) >> 8;
+            w[p] |= ((uint32_t)(dv & 0xff)) << (8 * r);
+          }
+          w[0] |= ((uint32_t)((int)v & 0xff)) << (8 * r);  // |v| <= 65 here
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < OZ_S; ++p) dig[p][ii][kq] = w[p];
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < OZ_S * 64 * 4; it += 256) {
+      const int c = it & 3, ii = (it >> 2) & 63, p = it >> 8;
+      const int i = i0 + ii;
+      const int64_t k = k0 + c * 16;
+      if (i >= mp || k >= kpad) continue;
+      uint4 v;
+      v.x = dig[p][ii][c * 4 + 0];
+      v.y = dig[p][ii][c * 4 + 1];
+      v.z = dig[p][ii][c * 4 + 2];
+      v.w = dig[p][ii][c * 4 + 3];
+      *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * mp + i) * kpad + k) = v;
+    }
+    __syncthreads();
   }
 }
 
@@ -405,9 +427,10 @@ inline bool oz_supported(int M, int64_t K, int nbatch) {
 // Exponents + K-major slices of a batch of column-major matrices (rows padded to in.mpad()).
 inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cudaStream_t st) {
   const int mp = in.mpad();
-  oz_rowexp_kernel<<<dim3((mp + 255) / 256, in.nbatch), 256, 0, st>>>(in, E);
+  oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E);
   RP_LAUNCH_CHECK("ozaki rowexp");
-  oz_slice_kernel<<<dim3((unsigned)(kpad / 64), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(in, E, slices, kpad);
+  oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(in, E, slices,
+                                                                                                  kpad);
   RP_LAUNCH_CHECK("ozaki slice");
   return RP_OK;
 }
@@ -703,7 +726,7 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   const int grid = a.total_tiles < sms ? a.total_tiles : sms;
   cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
   {
-    ProfScope prof("holdout_gemm", st);
+    ProfScope prof("oz_holdout", st);
     oz_dotb_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ta, tb, a);
   }
   RP_LAUNCH_CHECK("ozaki holdout");
