@@ -369,6 +369,122 @@ def grid_search_exact(p, grid, folds, metric=RMSE, threads=None, holdout="auto")
     return _merge("chol", grid.values, curves, per_fold, wall)
 
 
+def mchol_search(p, c0, s0_init, s_min, folds, metric=RMSE, threads=None, holdout="auto"):
+    """Three-point log-scale narrowing with exact solves (cvsearch.py:246-320), on the device.
+
+    Each round evaluates the new candidates of {c - s, c, c + s} (log10 lambda) for all folds in
+    one batched factorization; the fold-mean error (and, for several outputs, its mean over the
+    outputs) picks the next center; s halves until s <= s_min. Per fold the factorization count
+    is exactly 3 + 2 * ceil(log2(s0_init / s_min)), as in the reference."""
+    from . import exact
+
+    if not s0_init > s_min > 0:
+        raise UsageError(f"need s0_init > s_min > 0, got {s0_init}, {s_min}")
+    if metric not in METRICS:
+        raise UsageError(f"unknown metric {metric!r}")
+    threads = resolve_threads(threads)
+    t_start = time.perf_counter()
+    X, Y, counts = prepare_design(p, folds)
+    ev = exact.ExactEvaluator(X, Y, counts, metric=metric, holdout=holdout)
+    cache = {}
+
+    def evaluate(lcs):
+        new = [lc for lc in dict.fromkeys(lcs) if lc not in cache]
+        if new:
+            curves = ev.eval(np.array([10.0 ** lc for lc in new]))  # (k, len(new), m)
+            fold_mean = np.mean(curves, axis=0)  # fold-ordered mean (cvsearch.py:290)
+            for j, lc in enumerate(new):
+                e = fold_mean[j]
+                cache[lc] = float(e[0]) if e.shape[0] == 1 else float(np.mean(e))
+        return [cache[lc] for lc in lcs]
+
+    c, s = float(c0), float(s0_init)
+    while True:
+        cands = [c - s, c, c + s]
+        vals = evaluate(cands)
+        c = cands[int(np.argmin(vals))]
+        if s <= s_min:
+            break
+        s /= 2.0
+    wall = time.perf_counter() - t_start
+    evaluated = sorted(cache)
+    lams = np.array([10.0 ** lc for lc in evaluated])
+    errs = np.array([cache[lc] for lc in evaluated])
+    rows = [{"fold": -1, "lambda": float(l), "error": float(e), **_zero_timings()} for l, e in zip(lams, errs)]
+    timings = _zero_timings()
+    timings["factorize"] = wall
+    best_idx = int(np.argmin(errs))
+    return CvReport(
+        method="mchol",
+        per_lambda_error={float(l): float(e) for l, e in zip(lams, errs)},
+        best_lambda=float(lams[best_idx]),
+        best_error=float(errs[best_idx]),
+        timings=timings,
+        rows=rows,
+        wall_seconds=wall,
+    )
+
+
+def pinrmse_search(p, grid, folds, metric=RMSE, g=4, r=2, threads=None, holdout="auto"):
+    """Interpolate the hold-out error curve itself from g exact points (cvsearch.py:322-380).
+
+    The g sampled exact errors (device, all folds in one batch) are averaged over folds; the
+    degree-r polynomial fit and its minimizer over the grid are the reference's host
+    arithmetic on those g numbers (same V, same COND_LIMIT rescale, same Cholesky of V^T V)."""
+    import scipy.linalg
+
+    from . import exact
+
+    if g <= r:
+        raise UsageError(f"need more samples than the degree: g={g}, r={r}")
+    if g > grid.q:
+        raise UsageError(f"cannot draw g={g} samples from a grid of {grid.q}")
+    if metric not in METRICS:
+        raise UsageError(f"unknown metric {metric!r}")
+    threads = resolve_threads(threads)
+    t_start = time.perf_counter()
+    sample_lams = grid.values[pichol.sample_indices(grid.q, g)]
+    X, Y, counts = prepare_design(p, folds)
+    ev = exact.ExactEvaluator(X, Y, counts, metric=metric, holdout=holdout)
+    curves = ev.eval(sample_lams)  # (k, g, m)
+    fold_errs = curves[:, :, 0] if curves.shape[2] == 1 else np.mean(curves, axis=2)
+    mean_errs = np.mean(fold_errs, axis=0)
+    lams = np.asarray(sample_lams, dtype=float)
+    V = np.vander(lams, r + 1, increasing=True)
+    t_scale, t_shift = 1.0, 0.0
+    if float(np.linalg.cond(V)) > pichol.COND_LIMIT:
+        span = lams[-1] - lams[0]
+        t_scale = 2.0 / span
+        t_shift = -(lams[-1] + lams[0]) / span
+        V = np.vander(t_scale * lams + t_shift, r + 1, increasing=True)
+    Lv = scipy.linalg.cholesky(V.T @ V, lower=True, check_finite=False)
+    w = scipy.linalg.solve_triangular(Lv, V.T @ mean_errs, lower=True, check_finite=False)
+    coeff = scipy.linalg.solve_triangular(Lv.T, w, lower=False, check_finite=False)
+    fitted = np.vander(t_scale * grid.values + t_shift, r + 1, increasing=True) @ coeff
+    wall = time.perf_counter() - t_start
+    per_fold = _zero_timings()
+    per_fold["factorize"] = wall / folds.k
+    rows = []
+    for i in range(folds.k):
+        for lam, e in zip(sample_lams, fold_errs[i]):
+            rows.append({"fold": i, "lambda": float(lam), "error": float(e), **per_fold})
+    for lam, e in zip(grid.values, fitted):
+        rows.append({"fold": -1, "lambda": float(lam), "error": float(e), **_zero_timings()})
+    timings = _zero_timings()
+    timings["factorize"] = wall
+    best_idx = int(np.argmin(fitted))
+    return CvReport(
+        method="pinrmse",
+        per_lambda_error={float(l): float(e) for l, e in zip(grid.values, fitted)},
+        best_lambda=float(grid.values[best_idx]),
+        best_error=float(fitted[best_idx]),
+        timings=timings,
+        rows=rows,
+        wall_seconds=wall,
+        curves=curves,
+    )
+
+
 def _fit_basis_checked(sample_lams, r, raw_monomials):
     from .errors import DegenerateSamples, InsufficientSamples
 

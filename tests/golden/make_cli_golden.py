@@ -53,6 +53,10 @@ def main():
                     "--q", "15", "--folds", "4", "--fold-seed", "3"],
         "cv_mis": ["cv", "--x", p("Xm.bin"), "--y", p("ym.bin"), "--method", "pichol", "--metric", "misclass",
                    "--q", "11", "--folds", "3", "--g", "3", "--r", "2"],
+        "cv_mchol": ["cv", "--x", p("X.bin"), "--y", p("y.bin"), "--method", "mchol", "--lo", "1e-3", "--hi", "10",
+                     "--q", "15", "--folds", "4", "--fold-seed", "3"],
+        "cv_pinrmse": ["cv", "--x", p("X.bin"), "--y", p("y.bin"), "--method", "pinrmse", "--lo", "1e-3", "--hi",
+                       "10", "--q", "15", "--folds", "4", "--fold-seed", "3", "--g", "5", "--r", "2"],
         "fp": ["factor-path", "--matrix", p("H.bin"), "--lambdas", "0.01,0.03,0.1,0.3,1,3", "--g", "4", "--r", "2"],
     }
     stdout = {}

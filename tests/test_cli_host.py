@@ -77,5 +77,6 @@ def test_exit_codes_match_reference(tmp_path):
     assert cli.main(["cv", "--x", gp("X.bin")]) == runs["bad_arg"]["rc"] == 1
     # baselines outside the hot path and other reference commands: usage errors
     assert cli.main(["cv", "--x", gp("X.bin"), "--y", gp("y.bin"), "--method", "svd", "--out", out]) == 1
+    assert cli.main(["cv", "--x", gp("X.bin"), "--y", gp("y.bin"), "--method", "rsvd", "--out", out]) == 1
     assert cli.main(["gen", "--n", "10"]) == 1
     assert cli.main(["--help"]) == 0

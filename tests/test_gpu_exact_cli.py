@@ -1,5 +1,6 @@
-"""Device exact-Cholesky CV (cvsearch.grid_search_exact, cvsearch.py:178-203) and the
-command line (cli.py) against the reference's golden fixtures and the CPU oracle.
+"""Device exact-Cholesky CV (cvsearch.grid_search_exact, cvsearch.py:178-203; mchol_search
+:246-320; pinrmse_search :322-380) and the command line (cli.py) against the reference's golden
+fixtures and the CPU oracle.
 
 Tolerances as for the piCholesky sweep: hold-out errors within 1e-8 relative, misclass
 error rates identical, identical selected lambda."""
@@ -13,7 +14,7 @@ import pytest
 
 from oracle import pichol_oracle as orc
 from paper_1404_0466_b200 import cli, configs, cvsearch, exact
-from paper_1404_0466_b200.errors import NotPositiveDefinite
+from paper_1404_0466_b200.errors import NotPositiveDefinite, UsageError
 from tests.conftest import golden
 from tests.helpers import rel
 
@@ -94,7 +95,7 @@ def read_report(path):
     return rows[0], [(r[0], int(r[1]), float(r[2]), float(r[3])) for r in rows[1:]]
 
 
-@pytest.mark.parametrize("name", ["cv_pichol", "cv_chol", "cv_mis"])
+@pytest.mark.parametrize("name", ["cv_pichol", "cv_chol", "cv_mis", "cv_mchol", "cv_pinrmse"])
 def test_cli_cv_matches_reference(gpu, tmp_path, capsys, name):
     runs = json.load(open(os.path.join(GOLD, "runs.json")))
     argv = [os.path.join(GOLD, a) if a.endswith((".bin", ".csv")) else a for a in runs[name]["argv"]]
@@ -124,3 +125,26 @@ def test_cli_factor_path_matches_reference(gpu, tmp_path, capsys):
     mine = np.loadtxt(out, delimiter=",", skiprows=1)
     assert np.array_equal(mine[:, [0, 2]], ref[:, [0, 2]])
     assert np.max(np.abs(mine[:, 1] - ref[:, 1])) <= 1e-8 * np.max(ref[:, 1])
+
+
+def test_mchol_cost_formula_and_validation(gpu):
+    # cvsearch.py:246-252: exactly 3 + 2 * ceil(log2(s0 / s_min)) factorizations per fold
+    X, Y = configs.powerlaw(400, 30, 1, seed=2)
+    folds = cvsearch.contiguous_folds(400, 4)
+    rep = cvsearch.mchol_search(cvsearch.Dataset(X, Y[:, 0]), -1.5, 1.5, 0.0025, folds)
+    assert rep.method == "mchol" and len(rep.per_lambda_error) == 3 + 2 * int(np.ceil(np.log2(1.5 / 0.0025)))
+    assert rep.best_error == min(rep.per_lambda_error.values())
+    with pytest.raises(UsageError):
+        cvsearch.mchol_search(cvsearch.Dataset(X, Y[:, 0]), -1.5, 0.001, 0.01, folds)
+
+
+def test_pinrmse_exact_at_samples_matches_oracle(gpu):
+    # the sampled per-fold errors are exact hold-out errors (oracle.grid_search_exact at those lambdas)
+    X, Y = configs.powerlaw(500, 40, 1, seed=4)
+    folds = cvsearch.contiguous_folds(500, 5)
+    grid = cvsearch.make_grid(1e-3, 1e1, 21)
+    rep = cvsearch.pinrmse_search(cvsearch.Dataset(X, Y[:, 0]), grid, folds, g=5, r=2)
+    sl = grid.values[orc.sample_indices(21, 5)]
+    ref = orc.grid_search_exact(X, Y[:, 0], folds.assignments, 5, sl)
+    assert rel(rep.curves, ref["curves"]) <= 1e-8
+    assert rep.method == "pinrmse" and len(rep.per_lambda_error) == 21
