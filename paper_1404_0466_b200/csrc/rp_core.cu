@@ -477,22 +477,29 @@ __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, 
 }
 
 // bc[f][n] = sum_i W[i][n] * C_f[i][o]
-__global__ void holdout_bc_kernel(const double* W, int64_t ldw, int64_t w_fold_stride, const double* Cf,
-                                  int64_t c_stride, int d, int m, int N, double* bc) {
-  const int f = blockIdx.y;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
-  const int o = n % m;
-  const double* w = W + f * w_fold_stride + n;
-  const double* c = Cf + f * c_stride + (int64_t)o * d;
-  double s0 = 0.0, s1 = 0.0;
-  int i = 0;
-  for (; i + 2 <= d; i += 2) {
-    s0 = fma(w[(int64_t)i * ldw], c[i], s0);
-    s1 = fma(w[(int64_t)(i + 1) * ldw], c[i + 1], s1);
+// bc[f][n] = sum_i W[i][n] * C_f[i][o]: CTA = 32 columns x 8 row groups (rows i = g mod 8,
+// coalesced 256-byte row segments), the 8 partials combined in a fixed order.
+__global__ void __launch_bounds__(256) holdout_bc_kernel(const double* W, int64_t ldw, int64_t w_fold_stride,
+                                                         const double* Cf, int64_t c_stride, int d, int m, int N,
+                                                         double* bc) {
+  __shared__ double red[8][32];
+  const int f = blockIdx.y, lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int n = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (n < N) {
+    const int o = n % m;
+    const double* w = W + f * w_fold_stride + n;
+    const double* c = Cf + f * c_stride + (int64_t)o * d;
+#pragma unroll 4
+    for (int i = g; i < d; i += 8) s = fma(w[(int64_t)i * ldw], c[i], s);
   }
-  if (i < d) s0 = fma(w[(int64_t)i * ldw], c[i], s0);
-  bc[(int64_t)f * N + n] = s0 + s1;
+  red[g][lane] = s;
+  __syncthreads();
+  if (g == 0 && n < N) {
+    double t = red[0][lane];
+    for (int r = 1; r < 8; ++r) t += red[r][lane];
+    bc[(int64_t)f * N + n] = t;
+  }
 }
 
 __global__ void select_kernel(const double* curves, int k, int q, int m, double* mean, int* best) {
@@ -1052,7 +1059,7 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
     int rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial,
                         reinterpret_cast<uint8_t*>(work) + base, st);
     if (rc) return rc;
-    holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
+    holdout_bc_kernel<<<dim3((N + 31) / 32, nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
     RP_LAUNCH_CHECK("holdout bc");
     holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, 2 * mtiles, N, m, n_val, RP_METRIC_RMSE,
                                                                yy, bc, 2.0, curves);
@@ -1083,7 +1090,7 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
     rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
   }
   if (rc) return rc;
-  holdout_bc_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
+  holdout_bc_kernel<<<dim3((N + 31) / 32, nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
   RP_LAUNCH_CHECK("holdout bc");
   holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy, bc,
                                                              a.tri_a ? 2.0 : 1.0, curves);

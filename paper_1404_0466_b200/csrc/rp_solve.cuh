@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 
   for (int step = 0; step < a.nt; ++step) {
     const int I = BWD ? (a.nt - 1 - step) : step;
-    const int nslab = 4 * (BWD ? (a.nt - 1 - I) : I);
+    const int nslab = (a.dbg & 4) ? 0 : 4 * (BWD ? (a.nt - 1 - I) : I);  // dbg 4: diagonal steps only
 #pragma unroll
     for (int i = 0; i < LH; ++i)
 #pragma unroll
