@@ -196,6 +196,32 @@ RP_DEVINL void oz_tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint
       : "memory");
 }
 
+RP_DEVINL void oz_tma_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+RP_DEVINL void oz_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+RP_DEVINL uint32_t oz_cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
+RP_DEVINL void oz_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 RP_DEVINL void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
@@ -219,6 +245,18 @@ RP_DEVINL void oz_tile(int lin, int per, int& b, int& I, int& J) {
   J = t - i * (i + 1) / 2;
 }
 
+// Pairs of lower tiles (I, 2jp), (I, 2jp + 1) with 2jp <= I: floor(I/2) + 1 pairs in row I.
+RP_DEVINL void oz_pair(int lin, int per, int& b, int& I, int& jp) {
+  b = lin / per;
+  int t = lin - b * per, i = 0;
+  while (t >= (i >> 1) + 1) {
+    t -= (i >> 1) + 1;
+    ++i;
+  }
+  I = i;
+  jp = t;
+}
+
 struct OzArgs {
   const int* E;      // [nbatch][M]
   double* C;         // C_b at C + b * cstride, column-major, leading dimension ldc
@@ -228,6 +266,12 @@ struct OzArgs {
   int64_t kpad, kchunk;
 };
 
+// CL = 2: a cluster of two CTAs computes tiles (I, 2jp) and (I, 2jp + 1), which share the
+// A_I operand: each CTA loads half of the A_I slices and multicasts them to both, and the
+// stage is released to the producers by both CTAs' MMAs (commit multicast), halving the A
+// traffic from L2. The upper tile of a pair on the diagonal (J = I + 1) is computed but not
+// stored.
+template <int CL>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
     oz_syrk_kernel(const __grid_constant__ CUtensorMap tm, OzArgs a) {
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
@@ -241,10 +285,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nchunks = (int)((a.kpad + a.kchunk - 1) / a.kchunk);
 
+  const int rank = CL == 2 ? (int)oz_cluster_rank() : 0;
+  const int unit0 = CL == 2 ? blockIdx.x / 2 : blockIdx.x, ustep = CL == 2 ? gridDim.x / 2 : gridDim.x;
+  const int mt = a.M / OZ_BM;
+  // work unit -> (b, I, J) of this CTA; valid = a lower tile inside the matrix
+  auto unit_tile = [&](int u, int& b, int& I, int& J) {
+    if (CL == 2) {
+      int jp;
+      oz_pair(u, a.per, b, I, jp);
+      J = 2 * jp + rank;
+    } else {
+      oz_tile(u, a.per, b, I, J);
+    }
+    return J <= I;
+  };
+
   if (tid == 0) {
     for (int s = 0; s < OZ_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);  // CL == 2: released by both CTAs' MMAs
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 4);
@@ -256,6 +315,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   }
   oz_fence_before();
   __syncthreads();
+  if (CL == 2) oz_cluster_sync();  // the peer's barriers exist before any multicast
   oz_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -263,22 +323,28 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
         int b, I, J;
-        oz_tile(tile, a.per, b, I, J);
-        const int rowA = b * OZ_S * a.M + I * OZ_BM, rowB = b * OZ_S * a.M + J * OZ_BM;
+        unit_tile(u, b, I, J);
+        const int Jl = J < mt ? J : I;  // past the last column tile: load a valid (unused) tile
+        const int rowA = b * OZ_S * a.M + I * OZ_BM, rowB = b * OZ_S * a.M + Jl * OZ_BM;
         for (int pass = 1; pass >= 0; --pass) {
           const int ns = pass ? OZ_S : OZ_GP;  // slices the pass reads
+          const int half = (ns + 1) / 2;
+          const int pa0 = CL == 2 ? rank * half : 0, pa1 = CL == 2 ? (rank ? ns : half) : ns;
           for (int64_t k = 0; k < a.kpad; k += OZ_BK, ++it) {
             const int st = it % OZ_STAGES;
             mbar_wait(&empty[st], ((it / OZ_STAGES) & 1) ^ 1);
             mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * OZ_SLICE));
             uint8_t* sa = smem + st * OZ_STAGE;
             uint8_t* sb = sa + OZ_S * OZ_SLICE;
-            for (int p = 0; p < ns; ++p) {
-              oz_tma_2d(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.M, &full[st]);
-              oz_tma_2d(sb + p * OZ_SLICE, &tm, (int)k, rowB + p * a.M, &full[st]);
+            for (int p = pa0; p < pa1; ++p) {
+              if (CL == 2)
+                oz_tma_2d_mc(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.M, &full[st], (uint16_t)3);
+              else
+                oz_tma_2d(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.M, &full[st]);
             }
+            for (int p = 0; p < ns; ++p) oz_tma_2d(sb + p * OZ_SLICE, &tm, (int)k, rowB + p * a.M, &full[st]);
           }
         }
       }
@@ -287,7 +353,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       int it = 0, item = 0;
-      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
         for (int pass = 1; pass >= 0; --pass) {
           const int g0 = pass * OZ_GP;
           for (int ch = 0; ch < nchunks; ++ch, ++item) {
@@ -311,7 +377,11 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                   oz_mma(tmem + (uint32_t)((g - g0) * 128), oz_desc_sw32(sa + p * OZ_SLICE),
                          oz_desc_sw32(sb + q * OZ_SLICE), (first && p == 0) ? 0u : 1u);
                 }
-              oz_commit(&empty[st]);  // frees the stage once these MMAs have read it
+              // frees the stage (in both CTAs of a pair) once these MMAs have read it
+              if (CL == 2)
+                oz_commit_mc(&empty[st], (uint16_t)3);
+              else
+                oz_commit(&empty[st]);
             }
             oz_commit(tfull);
           }
@@ -323,9 +393,9 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const int quarter = warp & 3;
     const int row_in_tile = quarter * 32 + lane;
     int item = 0;
-    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
+    for (int u = unit0; u < a.total_tiles; u += ustep) {
       int b, I, J;
-      oz_tile(tile, a.per, b, I, J);
+      const bool valid = unit_tile(u, b, I, J);
       const int i = I * OZ_BM + row_in_tile;
       const int* Eb = a.E + (int64_t)b * a.M;
       const int ei = Eb[i];
@@ -352,6 +422,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
             }
             // read-modify-write of this 32-column chunk: every load is issued before any store
             // (a store could alias a later load otherwise and serialise 32 global round trips)
+            if (!valid) continue;  // the upper tile of a diagonal pair: accumulators drained only
             double* dst0 = Cb + (int64_t)(J * OZ_BM + h * 32) * a.ldc + i;
             double old[32];
             if (!first_item) {
@@ -380,6 +451,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     }
   }
   __syncthreads();
+  if (CL == 2) oz_cluster_sync();  // no CTA leaves while its peer may still signal it
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
@@ -453,19 +525,57 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   a.cstride = cstride;
   a.M = in.M;
   const int mt = in.M / OZ_BM;
-  a.per = mt * (mt + 1) / 2;
-  a.total_tiles = a.per * in.nbatch;
   a.subtract = subtract ? 1 : 0;
   a.kpad = kpad;
   a.kchunk = oz_kchunk(kpad);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // RP_OZAKI_CLUSTER=1: 2-CTA clusters sharing A_I by multicast. Halves the A traffic from L2
+  // but measured slower at c4 (Gram kernel 21.3 vs 20.1 ms: the pair runs in lockstep and
+  // wastes the diagonal pair's upper tile); the kernel is not L2-bound (a 4th stage also
+  // changed nothing), so the default is independent CTAs.
+  static const bool cluster = [] {
+    const char* e = getenv("RP_OZAKI_CLUSTER");
+    return e && e[0] == '1';
+  }();
+  if (cluster && mt >= 2) {
+    // pairs of tiles sharing A_I on 2-CTA clusters (A multicast)
+    a.per = 0;
+    for (int i = 0; i < mt; ++i) a.per += i / 2 + 1;
+    a.total_tiles = a.per * in.nbatch;
+    auto k = oz_syrk_kernel<2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.dynamicSmemBytes = OZ_SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(sms);
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess || clusters < 1) clusters = sms / 2;
+    (void)cudaGetLastError();
+    if (clusters > a.total_tiles) clusters = a.total_tiles;
+    cfg.gridDim = dim3(2 * clusters);
+    ProfScope prof(prof_name, st);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, tm, a);
+    if (e != cudaSuccess) return cuda_status(e, "ozaki syrk (cluster)");
+    count_launch();
+    return RP_OK;
+  }
+  a.per = mt * (mt + 1) / 2;
+  a.total_tiles = a.per * in.nbatch;
   const int grid = a.total_tiles < sms ? a.total_tiles : sms;
-  cudaFuncSetAttribute(oz_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+  cudaFuncSetAttribute(oz_syrk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
   {
     ProfScope prof(prof_name, st);
-    oz_syrk_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
+    oz_syrk_kernel<1><<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
   }
   RP_LAUNCH_CHECK("ozaki syrk");
   return RP_OK;
