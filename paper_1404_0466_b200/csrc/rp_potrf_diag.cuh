@@ -22,6 +22,35 @@ constexpr int PD_LDD = 24;  // stride of the 16 x 16 inverse blocks
 constexpr int PD_THREADS = 512;
 constexpr size_t PD_SMEM = sizeof(double) * (PD_NB * PD_LDA + 2 * 8 * 16 * PD_LDD + 16 * 16 * 8);
 
+// Register-resident 16 x 16 dpotf2 step J (lane i < 16 holds row i; column J of L broadcast
+// with shuffles), unrolled at compile time so `row` never leaves registers. rinv[J] = 1/L(J,J).
+template <int J>
+RP_DEVINL void pd_factor_step(double (&row)[16], int ri, int& bad, double* rinv) {
+  double ajj = __shfl_sync(0xffffffffu, row[J], J);
+  if (!bad && !(ajj > 0.0)) bad = J + 1;  // uniform across the warp
+  if (bad) ajj = 1.0;                       // keep the (discarded) arithmetic finite
+  const double ljj = sqrt(ajj), rl = 1.0 / ljj;
+  if (ri > J) row[J] *= rl;
+  if (ri == J) row[J] = ljj;
+  if ((threadIdx.x & 31) == 0) rinv[J] = rl;
+#pragma unroll
+  for (int c = J + 1; c < 16; ++c) {
+    const double lcj = __shfl_sync(0xffffffffu, row[J], c);  // L(c, J)
+    if (ri >= c) row[c] = fma(-row[J], lcj, row[c]);
+  }
+  if constexpr (J + 1 < 16) pd_factor_step<J + 1>(row, ri, bad, rinv);
+}
+
+// Row I of column c of D^-1 (forward substitution D x = e_c), x in registers.
+template <int I>
+RP_DEVINL void pd_inv_step(double (&x)[16], const double* D, const double* rinv, int c) {
+  double s = (I == c) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < I; ++k) s = fma(-D[k * PD_LDA + I], x[k], s);
+  x[I] = (I < c) ? 0.0 : s * rinv[I];
+  if constexpr (I + 1 < 16) pd_inv_step<I + 1>(x, D, rinv, c);
+}
+
 __global__ void __launch_bounds__(PD_THREADS, 1) potrf_diag_dmma_kernel(double* A, int d, int64_t stride, int k0,
                                                                        double* inv, int* info) {
   extern __shared__ __align__(16) double sm[];
@@ -76,24 +105,12 @@ __global__ void __launch_bounds__(PD_THREADS, 1) potrf_diag_dmma_kernel(double* 
       // register-resident 16 x 16 factor: lane i (< 16) holds row i; column j of L is
       // broadcast with shuffles (dpotf2 order: sqrt pivot, scale by the reciprocal, rank-1 update)
       const int ri = lane & 15;
+      double* rinv = scratch;  // 16 reciprocal pivots (warp 0's scratch; the inverse phase reuses it later)
       double row[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) row[c] = (c <= ri) ? D[c * PD_LDA + ri] : 0.0;
       int bad = 0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        double ajj = __shfl_sync(0xffffffffu, row[j], j);
-        if (!bad && !(ajj > 0.0)) bad = j + 1;  // uniform across the warp
-        if (bad) ajj = 1.0;                       // keep the (discarded) arithmetic finite
-        const double ljj = sqrt(ajj), rl = 1.0 / ljj;
-        if (ri > j) row[j] *= rl;
-        if (ri == j) row[j] = ljj;
-#pragma unroll
-        for (int c = j + 1; c < 16; ++c) {
-          const double lcj = __shfl_sync(0xffffffffu, row[j], c);  // L(c, j)
-          if (ri >= c) row[c] = fma(-row[j], lcj, row[c]);
-        }
-      }
+      pd_factor_step<0>(row, ri, bad, rinv);
       if (bad) {
         if (lane == 0) fail = k0 + b0 + bad;
       } else if (lane < 16) {
@@ -105,13 +122,7 @@ __global__ void __launch_bounds__(PD_THREADS, 1) potrf_diag_dmma_kernel(double* 
       if (fail == 0 && lane < 16) {  // column `lane` of D^-1: solve D x = e_c
         const int c = lane;
         double x[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          double s = (i == c) ? 1.0 : 0.0;
-#pragma unroll
-          for (int k = 0; k < i; ++k) s -= D[k * PD_LDA + i] * x[k];
-          x[i] = (i < c) ? 0.0 : s / D[i * PD_LDA + i];
-        }
+        pd_inv_step<0>(x, D, rinv, c);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           dinvN[(jb * 16 + i) * PD_LDD + c] = x[i];  // Dinv(i, c) at [k=i][n=c]
