@@ -89,7 +89,9 @@ int rp_symmetrize(double* G, int d, int64_t stride, int nmat, void* stream);
  *   Gsum = sum_b G_b (fixed order b = 0..nblocks-1), lower triangle
  *   A[f][s] = Gsum - G[folds[f]] + lams[s] * I   (lower triangle, d x d col-major)
  *   rhs[f]  = sum_b C_b - C[folds[f]]             (dp x m row-major, rows >= d zero)
- * Gsum: d*d workspace. A: nf*s*d*d. rhs: nf*dp*m.                            */
+ * Gsum: d*d workspace. A: nf*s*d*d. rhs: nf*dp*m.
+ * folds_host[f] = -1: nothing is subtracted (the held-out fold's block is not
+ * among the nblocks summed, e.g. the last fold before its block has arrived). */
 int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m, const int* folds_host,
                     int nf, const double* lams_host, int s, double* Gsum, double* A, double* rhs,
                     void* stream);

@@ -177,10 +177,10 @@ __global__ void fold_shift_kernel(const double* Gsum, const double* G, int d, in
   const int f = blockIdx.y;
   const int64_t n = (int64_t)d * d;
   const double* gs = Gsum + (int64_t)j * d;
-  const double* gf = G + fa.folds[f] * n + (int64_t)j * d;
+  const double* gf = fa.folds[f] >= 0 ? G + fa.folds[f] * n + (int64_t)j * d : nullptr;  // -1: none held out
   double* out = A + (int64_t)f * s * n + (int64_t)j * d;
   for (int i = j + threadIdx.x; i < d; i += blockDim.x) {
-    const double v = __ldcs(gs + i) - __ldcs(gf + i);
+    const double v = gf ? __ldcs(gs + i) - __ldcs(gf + i) : __ldcs(gs + i);
     for (int si = 0; si < s; ++si) __stcs(out + si * n + i, (i == j) ? v + fa.lams[si] : v);
   }
 }
@@ -194,7 +194,7 @@ __global__ void fold_rhs_kernel(const double* C, int nblocks, int d, int dp, int
   if (i < d) {
     double s = 0.0;
     for (int b = 0; b < nblocks; ++b) s += C[((int64_t)b * m + o) * d + i];
-    v = s - C[((int64_t)fa.folds[f] * m + o) * d + i];
+    v = fa.folds[f] >= 0 ? s - C[((int64_t)fa.folds[f] * m + o) * d + i] : s;
   }
   rhs[(int64_t)f * dp * m + e] = v;
 }
@@ -724,7 +724,7 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
   RP_REQUIRE(nf >= 1 && nf <= 64 && s >= 1 && s <= 32, "rp_fold_systems: nf=%d (<=64), s=%d (<=32)", nf, s);
   FoldSysArgs fa;
   for (int f = 0; f < nf; ++f) {
-    RP_REQUIRE(folds_host[f] >= 0 && folds_host[f] < nblocks, "rp_fold_systems: fold %d", folds_host[f]);
+    RP_REQUIRE(folds_host[f] >= -1 && folds_host[f] < nblocks, "rp_fold_systems: fold %d", folds_host[f]);
     fa.folds[f] = folds_host[f];
   }
   for (int i = 0; i < s; ++i) fa.lams[i] = lams_host[i];

@@ -124,8 +124,8 @@ class PicholEngine:
         nval = max(self.block_rows[f] for f in self.local_folds)
         mg = max(c1 - c0 for c0, c1 in self.groups)
         self.ws_hold = torch.empty((_lib.query("rp_holdout_workspace_size", nval, d, q, mg, 1 if not self.equal_blocks else nf),), **u8)
-        self.ws_solve = torch.empty((max(_lib.query("rp_eval_solve_workspace_size", d, self.r, nf, c1 - c0, q)
-                                         for c0, c1 in self.groups),), **u8)
+        self.ws_solve = torch.empty((max(_lib.query("rp_eval_solve_workspace_size", d, self.r, n, c1 - c0, q)
+                                         for c0, c1 in self.groups for n in {1, max(nf - 1, 1), nf}),), **u8)
 
     def device_bytes(self):
         tot = 0
@@ -137,12 +137,13 @@ class PicholEngine:
         return tot
 
     # ------------------------------------------------------------------ stages
-    def stage_gram(self, X, Y, block_ready=None):
+    def stage_gram(self, X, Y, block_ready=None, blocks=None):
         """Gram blocks. block_ready: optional {block: cuda.Event} -- the Gram of a block then waits
-        only for that block's upload, so the host->device copy of later blocks overlaps it."""
+        only for that block's upload, so the host->device copy of later blocks overlaps it.
+        blocks: a subset of this engine's Gram blocks (default all)."""
         d, m = self.d, self.m
         st = stream()
-        blocks = self.gram_blocks
+        blocks = self.gram_blocks if blocks is None else blocks
         contiguous = blocks == list(range(blocks[0], blocks[0] + len(blocks)))
         if self.equal_blocks and contiguous and block_ready is None:
             b0 = blocks[0]
@@ -163,32 +164,45 @@ class PicholEngine:
                 if self.holdout == "gram":
                     call("rp_col_sumsq", ptr(Y[off:]), m, rows, 1, m, ptr(self.yy[b]), st)
 
-    def stage_systems(self, sample_lams):
-        folds = np.ascontiguousarray(self.local_folds, dtype=np.int32)
+    def stage_systems(self, sample_lams, part=None, nblocks=None, holdout_block=True):
+        """Shifted systems of the local folds part = (i0, i1). nblocks: sum only the first nblocks
+        Gram blocks; holdout_block=False: the folds' own blocks are not among them (nothing is
+        subtracted: the last fold before its block has arrived)."""
+        i0, i1 = part if part is not None else (0, self.nf)
+        fl = self.local_folds[i0:i1] if holdout_block else [-1] * (i1 - i0)
+        folds = np.ascontiguousarray(fl, dtype=np.int32)
         lams = np.ascontiguousarray(sample_lams, dtype=np.float64)
-        call("rp_fold_systems", ptr(self.G), ptr(self.C), self.k, self.d, self.m, _lib.host_ptr(folds), self.nf,
-             _lib.host_ptr(lams), self.s, ptr(self.Gsum), ptr(self.A), ptr(self.rhs), stream())
+        nb = self.k if nblocks is None else nblocks
+        call("rp_fold_systems", ptr(self.G), ptr(self.C), nb, self.d, self.m, _lib.host_ptr(folds), i1 - i0,
+             _lib.host_ptr(lams), self.s, ptr(self.Gsum), ptr(self.A[i0]), ptr(self.rhs[i0]), stream())
+
+    def symmetrize_holdout_blocks(self):
         if self.holdout == "gram":
             for f in self.local_folds:
                 call("rp_symmetrize", ptr(self.G[f]), self.d, self.d * self.d, 1, stream())
 
-    def stage_factorize(self):
+    def stage_factorize(self, part=None):
+        i0, i1 = part if part is not None else (0, self.nf)
         d = self.d
-        call("rp_potrf_batched", ptr(self.A), d, d * d, self.nf * self.s, ptr(self.info), ptr(self.ws_potrf), stream())
+        call("rp_potrf_batched", ptr(self.A[i0]), d, d * d, (i1 - i0) * self.s, ptr(self.info[i0 * self.s:]),
+             ptr(self.ws_potrf), stream())
 
-    def stage_fit(self, Pmat, Vmat):
+    def stage_fit(self, Pmat, Vmat, part=None):
+        i0, i1 = part if part is not None else (0, self.nf)
         Pm = np.ascontiguousarray(Pmat, dtype=np.float64)
         Vm = np.ascontiguousarray(Vmat, dtype=np.float64)
-        call("rp_fit_tiles", ptr(self.A), self.d, self.s, self.nf, self.r, _lib.host_ptr(Pm), _lib.host_ptr(Vm),
-             ptr(self.theta), ptr(self.resid), ptr(self.ws_fit), stream())
+        call("rp_fit_tiles", ptr(self.A[i0]), self.d, self.s, i1 - i0, self.r, _lib.host_ptr(Pm), _lib.host_ptr(Vm),
+             ptr(self.theta[i0]), ptr(self.resid[i0:]), ptr(self.ws_fit), stream())
 
-    def stage_solve(self):
+    def stage_solve(self, part=None):
+        i0, i1 = part if part is not None else (0, self.nf)
         for gi, (c0, c1) in enumerate(self.groups):
             if len(self.groups) > 1:
-                self.rhs_g[gi].copy_(self.rhs[:, :, c0:c1])
+                self.rhs_g[gi][i0:i1].copy_(self.rhs[i0:i1, :, c0:c1])
             W = self.W[gi]
-            call("rp_eval_solve", ptr(self.theta), self.d, self.r, self.nf, ptr(self.rhs_g[gi]), c1 - c0,
-                 ptr(self.tvals), self.q, ptr(W), W.shape[2], ptr(self.flags[gi]), ptr(self.ws_solve), stream())
+            call("rp_eval_solve", ptr(self.theta[i0]), self.d, self.r, i1 - i0, ptr(self.rhs_g[gi][i0]), c1 - c0,
+                 ptr(self.tvals), self.q, ptr(W[i0]), W.shape[2], ptr(self.flags[gi][i0:]), ptr(self.ws_solve),
+                 stream())
 
     def stage_holdout(self, X, Y):
         st = stream()
@@ -261,6 +275,7 @@ class PicholEngine:
         if exchange_grams is not None:
             exchange_grams(self)
         self.stage_systems(sample_lams)
+        self.symmetrize_holdout_blocks()
         mark("assemble")
         self.stage_factorize()
         mark("factorize")

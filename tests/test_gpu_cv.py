@@ -151,3 +151,20 @@ def test_c4_full_size_fold0_matches_oracle(gpu):
     curves_d, _, best_d, _ = run_engine(cfg, X, Y, "direct")
     assert rel(curves_d, curves) <= 1e-9
     assert np.array_equal(best_d, best)
+
+
+@pytest.mark.parametrize("k", [3, 5])
+def test_session_streamed_upload_matches_resident_sweep(gpu, k):
+    """CvSession.run with pinned host inputs streams X per fold block (the Gram of block b
+    waits only for block b's copy); it must agree with the device-resident sweep and the oracle."""
+    import torch
+
+    X, Y = configs.powerlaw(600 * k, 96, 3, seed=k)
+    grid = cvsearch.make_grid(1e-3, 1e1, 23)
+    sess = cvsearch.CvSession([600] * k, 96, 3, grid.values, g=4, r=2)
+    curves_s, best_s = sess.run(torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory())
+    curves_r, best_r = sess.run(X, Y)
+    assert rel(curves_s, curves_r) <= 1e-12
+    assert np.array_equal(best_s, best_r)
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(600 * k, k), k, grid.values, g=4, r=2)
+    assert rel(curves_s, ref["curves"]) <= 1e-8
