@@ -85,16 +85,15 @@ int rp_col_sumsq(const double* Y, int64_t ldy, int64_t rows_per_block, int nbloc
 int rp_symmetrize(double* G, int d, int64_t stride, int nmat, void* stream);
 
 /* Per-fold shifted systems for the sampled-lambda factorizations
- * (pichol.py:105-107, `H + lam * eye`):
- *   Gsum = sum_b G_b (fixed order b = 0..nblocks-1), lower triangle
- *   A[f][s] = Gsum - G[folds[f]] + lams[s] * I   (lower triangle, d x d col-major)
- *   rhs[f]  = sum_b C_b - C[folds[f]]             (dp x m row-major, rows >= d zero)
- * Gsum: d*d workspace. A: nf*s*d*d. rhs: nf*dp*m.
- * folds_host[f] = -1: nothing is subtracted (the held-out fold's block is not
- * among the nblocks summed, e.g. the last fold before its block has arrived). */
+ * (pichol.py:105-107, `H + lam * eye`; H = X_tr^T X_tr of ridge.py:58 as a sum of fold blocks):
+ *   A[f][s] = sum_{b != folds[f]} G_b + lams[s] * I  (b = 0..nblocks-1 in order; lower triangle,
+ *                                                     d x d col-major)
+ *   rhs[f]  = sum_{b != folds[f]} C_b                 (dp x m row-major, rows >= d zero)
+ * A: nf*s*d*d. rhs: nf*dp*m. The sum of fold f does not depend on whether block f is among
+ * the nblocks, so a fold can be assembled from the other folds' blocks before its own block
+ * exists (folds_host[f] >= nblocks or -1: nothing is left out). */
 int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m, const int* folds_host,
-                    int nf, const double* lams_host, int s, double* Gsum, double* A, double* rhs,
-                    void* stream);
+                    int nf, const double* lams_host, int s, double* A, double* rhs, void* stream);
 
 /* (2) Batched blocked Cholesky, lower, in place.  Replaces linalg.cholesky's
  * dpotrf (linalg.py:98) for the s sampled lambdas of every local fold.

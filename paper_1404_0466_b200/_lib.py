@@ -41,7 +41,7 @@ SIGNATURES = {
     "rp_gram_blocks": (_i, [_vp, _i64, _i64, _i, _i, _vp, _i64, _i, _vp, _vp, _vp, _vp]),
     "rp_col_sumsq": (_i, [_vp, _i64, _i64, _i, _i, _vp, _vp]),
     "rp_symmetrize": (_i, [_vp, _i, _i64, _i, _vp]),
-    "rp_fold_systems": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp, _vp]),
+    "rp_fold_systems": (_i, [_vp, _vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _vp]),
     "rp_potrf_workspace_size": (_sz, [_i, _i]),
     "rp_potrf_batched": (_i, [_vp, _i, _i64, _i, _vp, _vp, _vp]),
     "rp_fit_tiles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),

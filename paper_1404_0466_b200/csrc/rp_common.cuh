@@ -113,7 +113,7 @@ inline int cuda_status(cudaError_t e, const char* where) {
 // Kernel timing for the bench's roofline (rp_set_option("profile", 1)): CUDA events recorded on
 // the launching stream around selected kernels, summed by rp_profile_ms(name).
 bool prof_on();
-void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b);
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b, cudaStream_t st);
 cudaEvent_t prof_event();
 struct ProfScope {
   const char* name;
@@ -129,7 +129,7 @@ struct ProfScope {
     if (a) {
       cudaEvent_t b = prof_event();
       cudaEventRecord(b, st);
-      prof_push(name, a, b);
+      prof_push(name, a, b, st);
     }
   }
 };

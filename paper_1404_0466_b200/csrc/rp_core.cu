@@ -1,6 +1,8 @@
 // C-ABI entry points for the piCholesky CV path (everything except the fused eval+solve,
 // which lives in rp_solve.cu). See include/ridgepath_b200.h for the contract and the
 // reference routine each entry point replaces.
+#include <map>
+#include <mutex>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -37,6 +39,7 @@ static bool g_profile = false;
 struct ProfRec {
   std::string name;
   cudaEvent_t a, b;
+  cudaStream_t st;
 };
 static std::vector<ProfRec> g_prof;
 bool prof_on() { return g_profile; }
@@ -45,7 +48,7 @@ cudaEvent_t prof_event() {
   cudaEventCreate(&e);
   return e;
 }
-void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b) { g_prof.push_back({name, a, b}); }
+void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b, cudaStream_t st) { g_prof.push_back({name, a, b, st}); }
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
@@ -159,43 +162,50 @@ struct FoldSysArgs {
   double lams[32];
 };
 
-__global__ void gram_sum_kernel(const double* G, int nblocks, int d, double* Gsum) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t n = (int64_t)d * d;
-  if (e >= n) return;
-  int i = (int)(e % d), j = (int)(e / d);
-  if (i < j) return;
-  double s = 0.0;
-  for (int b = 0; b < nblocks; ++b) s += G[b * n + e];
-  Gsum[e] = s;
-}
-
-// One pass per fold: H_f = Gsum - G_f read once, all s shifted copies written (lower triangle,
-// column by column so the threads of a block stay on contiguous rows).
-__global__ void fold_shift_kernel(const double* Gsum, const double* G, int d, int s, FoldSysArgs fa, double* A) {
+// Leave-one-out sums, one pass over the Gram blocks for all folds of the call:
+//   A[f][s] = sum_{b != folds[f]} G_b + lams[s] I  (fixed order b = 0..nblocks-1, lower triangle)
+// Each element's nblocks values are read once (registers when nblocks <= KB) and every fold's sum
+// is formed directly -- no G_total - G_f cancellation, and the sum of a fold is bit-identical
+// whether or not its own block is among the nblocks (the streamed path factors the last fold
+// before its block has arrived). Column by column so the threads of a block stay on contiguous rows.
+template <int KB>
+__global__ void fold_shift_kernel(const double* G, int nblocks, int d, int s, int nf, FoldSysArgs fa, double* A) {
   const int j = blockIdx.x;  // column
-  const int f = blockIdx.y;
   const int64_t n = (int64_t)d * d;
-  const double* gs = Gsum + (int64_t)j * d;
-  const double* gf = fa.folds[f] >= 0 ? G + fa.folds[f] * n + (int64_t)j * d : nullptr;  // -1: none held out
-  double* out = A + (int64_t)f * s * n + (int64_t)j * d;
+  const double* gj = G + (int64_t)j * d;
   for (int i = j + threadIdx.x; i < d; i += blockDim.x) {
-    const double v = gf ? __ldcs(gs + i) - __ldcs(gf + i) : __ldcs(gs + i);
-    for (int si = 0; si < s; ++si) __stcs(out + si * n + i, (i == j) ? v + fa.lams[si] : v);
+    double g[KB > 0 ? KB : 1];
+    if (KB > 0) {
+#pragma unroll
+      for (int b = 0; b < KB; ++b) g[b] = b < nblocks ? __ldcs(gj + b * n + i) : 0.0;
+    }
+    for (int f = 0; f < nf; ++f) {
+      const int hold = fa.folds[f];
+      double v = 0.0;
+      if (KB > 0) {
+#pragma unroll
+        for (int b = 0; b < KB; ++b)
+          if (b < nblocks && b != hold) v += g[b];
+      } else {
+        for (int b = 0; b < nblocks; ++b)
+          if (b != hold) v += gj[b * n + i];
+      }
+      double* out = A + (int64_t)f * s * n + (int64_t)j * d + i;
+      for (int si = 0; si < s; ++si) __stcs(out + si * n, (i == j) ? v + fa.lams[si] : v);
+    }
   }
 }
 
+// rhs[f] = sum_{b != folds[f]} C_b (fixed order), row-major dp x m, rows >= d zero.
 __global__ void fold_rhs_kernel(const double* C, int nblocks, int d, int dp, int m, FoldSysArgs fa, double* rhs) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;  // over dp*m, row-major (i, o)
   if (e >= dp * m) return;
   const int f = blockIdx.y;
   int i = e / m, o = e % m;
   double v = 0.0;
-  if (i < d) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += C[((int64_t)b * m + o) * d + i];
-    v = fa.folds[f] >= 0 ? s - C[((int64_t)fa.folds[f] * m + o) * d + i] : s;
-  }
+  if (i < d)
+    for (int b = 0; b < nblocks; ++b)
+      if (b != fa.folds[f]) v += C[((int64_t)b * m + o) * d + i];
   rhs[(int64_t)f * dp * m + e] = v;
 }
 
@@ -638,6 +648,34 @@ size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks) {
   return oz_workspace_bytes(d, rows_per_block, nblocks);
 }
 
+// Side streams (and fork/join events) per calling stream, created with the caller's priority:
+// work a call forks off (X^T Y beside the Gram, the Cholesky stream groups) stays independent of
+// other callers' and keeps the priority of the stream it was issued on.
+struct SideStreams {
+  cudaStream_t s[8];
+  cudaEvent_t fork, join[8];
+};
+
+static SideStreams* side_streams(cudaStream_t caller, int tag) {
+  static std::mutex mu;
+  static std::map<std::pair<cudaStream_t, int>, SideStreams> by_caller;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_pair(caller, tag);
+  auto it = by_caller.find(key);
+  if (it == by_caller.end()) {
+    int prio = 0;
+    cudaStreamGetPriority(caller, &prio);
+    SideStreams g{};
+    cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming);
+    for (int i = 0; i < 8; ++i) {
+      cudaStreamCreateWithPriority(&g.s[i], cudaStreamNonBlocking, prio);
+      cudaEventCreateWithFlags(&g.join[i], cudaEventDisableTiming);
+    }
+    it = by_caller.emplace(key, g).first;
+  }
+  return &it->second;
+}
+
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d, const double* Y,
                    int64_t ldy, int m, double* G, double* C, void* work, void* stream) {
   RP_REQUIRE(d >= 1 && nblocks >= 1 && rows_per_block >= 1 && ldx >= d, "rp_gram_blocks: bad sizes");
@@ -659,12 +697,13 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   const bool want_c = m > 0 && C != nullptr;
   if (want_c) RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
   const bool side = want_c && m <= 16 && aligned16(X) && ldx % 2 == 0 && !g_xty_gemm;
-  static cudaStream_t xs = nullptr;
-  static cudaEvent_t fork = nullptr, join = nullptr;
-  if (side && !xs) {
-    cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+  cudaStream_t xs = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (side) {
+    SideStreams* ss = side_streams(st, 0);
+    xs = ss->s[0];
+    fork = ss->fork;
+    join = ss->join[0];
   }
   if (side) {  // the side stream starts from the same point of `st` as the SYRK
     cudaError_t e = cudaEventRecord(fork, st);
@@ -720,20 +759,21 @@ int rp_col_sumsq(const double* Y, int64_t ldy, int64_t rows_per_block, int nbloc
 }
 
 int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m, const int* folds_host, int nf,
-                    const double* lams_host, int s, double* Gsum, double* A, double* rhs, void* stream) {
+                    const double* lams_host, int s, double* A, double* rhs, void* stream) {
   RP_REQUIRE(nf >= 1 && nf <= 64 && s >= 1 && s <= 32, "rp_fold_systems: nf=%d (<=64), s=%d (<=32)", nf, s);
+  RP_REQUIRE(nblocks >= 1 && d >= 1 && m >= 0, "rp_fold_systems: nblocks=%d d=%d m=%d", nblocks, d, m);
   FoldSysArgs fa;
   for (int f = 0; f < nf; ++f) {
-    RP_REQUIRE(folds_host[f] >= -1 && folds_host[f] < nblocks, "rp_fold_systems: fold %d", folds_host[f]);
+    RP_REQUIRE(folds_host[f] >= -1, "rp_fold_systems: fold %d", folds_host[f]);
     fa.folds[f] = folds_host[f];
   }
   for (int i = 0; i < s; ++i) fa.lams[i] = lams_host[i];
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t n = (int64_t)d * d;
-  gram_sum_kernel<<<grid1d(n), 256, 0, st>>>(G, nblocks, d, Gsum);
-  RP_LAUNCH_CHECK("gram_sum");
   if (A) {
-    fold_shift_kernel<<<dim3(d, nf), 256, 0, st>>>(Gsum, G, d, s, fa, A);
+    if (nblocks <= 16)
+      fold_shift_kernel<16><<<d, 256, 0, st>>>(G, nblocks, d, s, nf, fa, A);
+    else
+      fold_shift_kernel<0><<<d, 256, 0, st>>>(G, nblocks, d, s, nf, fa, A);
     RP_LAUNCH_CHECK("fold_shift");
   }
   if (rhs && m > 0) {
@@ -780,6 +820,20 @@ double rp_profile_ms(const char* name) {
   cudaDeviceSynchronize();
   double tot = 0.0;
   std::vector<ProfRec> keep;
+  // RP_PROF_TIMELINE=<path>: dump every record (name, stream, start, end in ms from the first)
+  if (name == nullptr && !g_prof.empty()) {
+    if (const char* path = getenv("RP_PROF_TIMELINE")) {
+      if (FILE* f = fopen(path, "w")) {
+        for (auto& r : g_prof) {
+          float t0 = 0.f, t1 = 0.f;
+          cudaEventElapsedTime(&t0, g_prof[0].a, r.a);
+          cudaEventElapsedTime(&t1, g_prof[0].a, r.b);
+          fprintf(f, "%s %p %.4f %.4f\n", r.name.c_str(), (void*)r.st, t0, t1);
+        }
+        fclose(f);
+      }
+    }
+  }
   for (auto& r : g_prof) {
     if (name == nullptr || r.name == name) {
       float ms = 0.f;
@@ -833,15 +887,12 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   uint8_t* ozbase = reinterpret_cast<uint8_t*>(work) +
                     ((sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB) + 1023) / 1024 * 1024;
   if (groups <= 1 || d <= CHOL_NB) return potrf_group(A, d, stride, batch, info, inv, ozg ? ozbase : nullptr, st);
-  static cudaStream_t gs[8] = {};
-  static cudaEvent_t fork = nullptr, join[8] = {};
-  if (!fork) {
-    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
-    for (int g = 0; g < 8; ++g) {
-      cudaStreamCreateWithFlags(&gs[g], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&join[g], cudaEventDisableTiming);
-    }
-  }
+  // group streams per calling stream: factorizations issued concurrently from different streams
+  // (the streamed sweep factors its last fold beside the others) stay independent
+  SideStreams* grp = side_streams(st, 1);
+  cudaStream_t* gs = grp->s;
+  cudaEvent_t fork = grp->fork;
+  cudaEvent_t* join = grp->join;
   e = cudaEventRecord(fork, st);
   if (e != cudaSuccess) return cuda_status(e, "potrf fork");
   int b0 = 0;
@@ -884,15 +935,19 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
         u.strideC = stride;
         u.alpha = -1.0;
         u.beta = 1.0;
+        ProfScope prof("chol_update", st);
         int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf panel update");
         if (rc) return rc;
       }
-      if (g_simple_diag) {
-        potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
-      } else {
-        potrf_diag_dmma_kernel<<<batch, PD_THREADS, PD_SMEM, st>>>(A, d, stride, k1, inv, info);
+      {
+        ProfScope prof("chol_diag", st);
+        if (g_simple_diag) {
+          potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
+        } else {
+          potrf_diag_dmma_kernel<<<batch, PD_THREADS, PD_SMEM, st>>>(A, d, stride, k1, inv, info);
+        }
+        RP_LAUNCH_CHECK("potrf_diag");
       }
-      RP_LAUNCH_CHECK("potrf_diag");
       const int rows = d - k1 - nb;
       if (rows > 0) {
         // L[k1+nb:d, k1:k1+nb] = A[...] * inv(L11)^T   (in place: each CTA owns whole rows, BN >= nb)
@@ -910,6 +965,7 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
         t.C = L21;
         t.ldc = d;
         t.strideC = stride;
+        ProfScope prof("chol_trsm", st);
         int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(t, batch, st, "potrf trsm");
         if (rc) return rc;
       }

@@ -513,8 +513,11 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   int* E = reinterpret_cast<int*>(work);
   int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(in.M, in.nbatch);
   const int64_t kpad = oz_kpad(in.K);
-  int rc = oz_prepare(in, E, slices, kpad, st);
-  if (rc) return rc;
+  {
+    ProfScope prof("oz_prep", st);
+    int rc = oz_prepare(in, E, slices, kpad, st);
+    if (rc) return rc;
+  }
   CUtensorMap tm;
   if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * in.M))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");

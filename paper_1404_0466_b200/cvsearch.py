@@ -292,8 +292,7 @@ class CvSession:
         pinned = isinstance(X, torch.Tensor) and X.is_pinned() and isinstance(Y, torch.Tensor) and Y.is_pinned()
         if pinned:
             ready = self.upload_streamed(X, Y)
-            Xd = self.X
-            curves, _, best = self.engine.sweep(Xd, self.Y, self.lams, self.P, self.V, self.tvals,
+            curves, _, best = self.engine.sweep(self.X, self.Y, self.lams, self.P, self.V, self.tvals,
                                                 exchange_grams=self._exchange, gather_curves=self._gather,
                                                 timings=timings, block_ready=ready)
         else:

@@ -94,7 +94,6 @@ class PicholEngine:
         self.G = torch.empty((k, d, d), **f64)
         self.C = torch.empty((k, m, d), **f64)  # C_b column-major d x m == (m, d) row-major
         self.yy = torch.empty((k, m), **f64)
-        self.Gsum = torch.empty((d, d), **f64)
         self.A = torch.empty((nf, s, d, d), **f64)
         self.theta = torch.empty((nf, tile_elems(d, self.P)), **f64)
         self.resid = torch.empty((nf,), **f64)
@@ -125,7 +124,7 @@ class PicholEngine:
         mg = max(c1 - c0 for c0, c1 in self.groups)
         self.ws_hold = torch.empty((_lib.query("rp_holdout_workspace_size", nval, d, q, mg, 1 if not self.equal_blocks else nf),), **u8)
         self.ws_solve = torch.empty((max(_lib.query("rp_eval_solve_workspace_size", d, self.r, n, c1 - c0, q)
-                                         for c0, c1 in self.groups for n in {1, max(nf - 1, 1), nf}),), **u8)
+                                         for c0, c1 in self.groups for n in {max(nf - 1, 1), nf}),), **u8)
 
     def device_bytes(self):
         tot = 0
@@ -164,45 +163,44 @@ class PicholEngine:
                 if self.holdout == "gram":
                     call("rp_col_sumsq", ptr(Y[off:]), m, rows, 1, m, ptr(self.yy[b]), st)
 
-    def stage_systems(self, sample_lams, part=None, nblocks=None, holdout_block=True):
-        """Shifted systems of the local folds part = (i0, i1). nblocks: sum only the first nblocks
-        Gram blocks; holdout_block=False: the folds' own blocks are not among them (nothing is
-        subtracted: the last fold before its block has arrived)."""
+    def stage_systems(self, sample_lams, part=None, nblocks=None):
+        """Shifted systems of the local folds part = (i0, i1): A_{f,s} = sum_{b != f} G_b + lam_s I.
+        nblocks: sum only the first nblocks Gram blocks (a fold whose own block is not among them
+        gets the same, bit-identical sum as with all blocks)."""
         i0, i1 = part if part is not None else (0, self.nf)
-        fl = self.local_folds[i0:i1] if holdout_block else [-1] * (i1 - i0)
-        folds = np.ascontiguousarray(fl, dtype=np.int32)
+        folds = np.ascontiguousarray(self.local_folds[i0:i1], dtype=np.int32)
         lams = np.ascontiguousarray(sample_lams, dtype=np.float64)
         nb = self.k if nblocks is None else nblocks
         call("rp_fold_systems", ptr(self.G), ptr(self.C), nb, self.d, self.m, _lib.host_ptr(folds), i1 - i0,
-             _lib.host_ptr(lams), self.s, ptr(self.Gsum), ptr(self.A[i0]), ptr(self.rhs[i0]), stream())
+             _lib.host_ptr(lams), self.s, ptr(self.A[i0]), ptr(self.rhs[i0]), stream())
 
     def symmetrize_holdout_blocks(self):
         if self.holdout == "gram":
             for f in self.local_folds:
                 call("rp_symmetrize", ptr(self.G[f]), self.d, self.d * self.d, 1, stream())
 
-    def stage_factorize(self, part=None):
+    def stage_factorize(self, part=None, ws=None):
         i0, i1 = part if part is not None else (0, self.nf)
         d = self.d
         call("rp_potrf_batched", ptr(self.A[i0]), d, d * d, (i1 - i0) * self.s, ptr(self.info[i0 * self.s:]),
-             ptr(self.ws_potrf), stream())
+             ptr(self.ws_potrf if ws is None else ws), stream())
 
-    def stage_fit(self, Pmat, Vmat, part=None):
+    def stage_fit(self, Pmat, Vmat, part=None, ws=None):
         i0, i1 = part if part is not None else (0, self.nf)
         Pm = np.ascontiguousarray(Pmat, dtype=np.float64)
         Vm = np.ascontiguousarray(Vmat, dtype=np.float64)
         call("rp_fit_tiles", ptr(self.A[i0]), self.d, self.s, i1 - i0, self.r, _lib.host_ptr(Pm), _lib.host_ptr(Vm),
-             ptr(self.theta[i0]), ptr(self.resid[i0:]), ptr(self.ws_fit), stream())
+             ptr(self.theta[i0]), ptr(self.resid[i0:]), ptr(self.ws_fit if ws is None else ws), stream())
 
-    def stage_solve(self, part=None):
+    def stage_solve(self, part=None, ws=None):
         i0, i1 = part if part is not None else (0, self.nf)
         for gi, (c0, c1) in enumerate(self.groups):
             if len(self.groups) > 1:
                 self.rhs_g[gi][i0:i1].copy_(self.rhs[i0:i1, :, c0:c1])
             W = self.W[gi]
             call("rp_eval_solve", ptr(self.theta[i0]), self.d, self.r, i1 - i0, ptr(self.rhs_g[gi][i0]), c1 - c0,
-                 ptr(self.tvals), self.q, ptr(W[i0]), W.shape[2], ptr(self.flags[gi][i0:]), ptr(self.ws_solve),
-                 stream())
+                 ptr(self.tvals), self.q, ptr(W[i0]), W.shape[2], ptr(self.flags[gi][i0:]),
+                 ptr(self.ws_solve if ws is None else ws), stream())
 
     def stage_holdout(self, X, Y):
         st = stream()

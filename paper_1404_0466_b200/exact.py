@@ -6,7 +6,7 @@ arbitrary lambdas: factor H_f + lambda I, solve, score. ``ExactEvaluator`` keeps
 Gram blocks resident and evaluates any set of lambdas for all folds at once, reusing the
 piCholesky kernels without interpolation:
 
-  rp_gram_blocks / rp_fold_systems   H_f = sum_b G_b - G_f, rhs_f, shifted by each lambda
+  rp_gram_blocks / rp_fold_systems   H_f = sum_{b != f} G_b, rhs_f, shifted by each lambda
   rp_potrf_batched                   up to 32 exact factors per call (folds x lambdas)
   rp_fit_tiles (s = 1, degree 0)     each factor packed into the tile layout as its own "model"
   rp_eval_solve (q = 1)              fused blocked forward/back substitution per factor
@@ -59,7 +59,6 @@ class ExactEvaluator:
             call("rp_col_sumsq", ptr(self.dY[off:]), m, rows, 1, m, ptr(self.yy[b]), st)
         if holdout == "gram":
             call("rp_symmetrize", ptr(self.G), d, d * d, k, st)
-        self.Gsum = _dev.empty((d, d))
         self.groups = [(c, min(c + MAX_M_PER_SOLVE, m)) for c in range(0, m, MAX_M_PER_SOLVE)]
         self._torch = torch
 
@@ -87,7 +86,7 @@ class ExactEvaluator:
         rhs = _dev.empty((nf, dp, m))
         fa = np.ascontiguousarray(folds, dtype=np.int32)
         call("rp_fold_systems", ptr(self.G), ptr(self.C), k, d, m, _lib.host_ptr(fa), nf, _lib.host_ptr(lams), nb,
-             ptr(self.Gsum), ptr(A), ptr(rhs), st)
+             ptr(A), ptr(rhs), st)
         info = _dev.zeros((nmod,), dtype=torch.int32)
         ws = _dev.workspace(_lib.query("rp_potrf_workspace_size", d, nmod))
         call("rp_potrf_batched", ptr(A), d, d * d, nmod, ptr(info), ptr(ws), st)
