@@ -235,9 +235,11 @@ constexpr int CHOL_NB = 128;
 static int CHOL_OB = [] {
   const char* e = getenv("RP_CHOL_OB");
   // measured at c4 with DMMA trailing updates: 384 -> 38.3 ms, 512 -> 37.4, 768 -> 36.8, 1024 -> 36.7;
-  // with tensor-core trailing updates (evals/s): 768 -> 15442, 1024 -> 15815, 1536 -> 15949, 2048 -> 15919
-  int v = e ? atoi(e) : 1536;
-  return v >= 128 && v % 128 == 0 ? v : 1536;
+  // with tensor-core trailing updates (evals/s): 768 -> 15442, 1024 -> 15815, 1536 -> 15949, 2048 -> 15919;
+  // once the tensor-core SYRK drained both passes before one C read-modify-write (factorize ms):
+  // 512 -> 24.3, 640 -> 24.6, 768 -> 22.4-24.0, 896 -> 23.2, 1024 -> 23.0-23.5, 1536 -> 26.1
+  int v = e ? atoi(e) : 768;
+  return v >= 128 && v % 128 == 0 ? v : 768;
 }();
 
 // Factor the NB x NB diagonal block at (k0, k0) of every batch matrix in shared memory

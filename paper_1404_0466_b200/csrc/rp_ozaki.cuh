@@ -21,8 +21,9 @@
 //                      warp 0 issues the TMA loads (SWIZZLE_32B boxes of 32 k x 128 rows, the
 //                      slices of A_I and A_J a pass needs), warp 1 allocates TMEM and issues the
 //                      tcgen05.mma (M = N = 128, K = 32) into 4 weight-group accumulators of
-//                      128 x 128 int32 (all 512 TMEM columns), warps 2-5 read TMEM (tcgen05.ld),
-//                      recombine in FP64 and add the tile into C. Only 4 groups fit in TMEM, so a
+//                      128 x 128 int32 (all 512 TMEM columns), warps 2-9 drain TMEM (tcgen05.ld)
+//                      into FP64 registers (64 columns per thread) and add the tile into C with a
+//                      single read-modify-write that overlaps the next tile's MMAs. Only 4 groups fit in TMEM, so a
 //                      tile runs two passes over K: groups 4..6 (all 7 slices), then 0..3
 //                      (slices 0..3). K is cut in chunks short enough that no int32 accumulator
 //                      can overflow (7 pairs x 128^2 x K_chunk < 2^31).
@@ -36,7 +37,8 @@ namespace rp {
 
 constexpr int OZ_S = 7;  // slices: balanced base-256 digits of a 54-bit fixed-point value
 constexpr int OZ_BM = 128, OZ_BK = 32, OZ_STAGES = 3, OZ_GP = 4;
-constexpr int OZ_THREADS = 192;  // producer, MMA, 4 epilogue warps
+constexpr int OZ_THREADS = 192;       // hold-out kernel: producer, MMA, 4 epilogue warps
+constexpr int OZ_SYRK_THREADS = 320;  // SYRK kernel: producer, MMA, 8 epilogue warps
 constexpr int OZ_SLICE = OZ_BM * OZ_BK;             // bytes of one 128 x 32 slice tile
 constexpr int OZ_STAGE = 2 * OZ_S * OZ_SLICE;        // A_I and A_J, all slices
 constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 128 + 4 * 32 * 8;
@@ -128,16 +130,23 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
           const int64_t k = k0 + kq * 4 + r;
           double x = xs[r];
           if (in.tri && k == i) x *= 0.5;  // exact
-          long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
-          // balanced base-256 digits, least significant first: d in [-128, 127], v = (v - d) / 256
-#pragma unroll
-          for (int p = OZ_S - 1; p >= 1; --p) {
-            const int dv = (int)(signed char)(v & 0xff);
-            v = (v - dv) >> 8;
-            w[p] |= ((uint32_t)(dv & 0xff)) << (8 * r);
-          }
-          w[0] |= ((uint32_t)((int)v & 0xff)) << (8 * r);  // |v| <= 65 here
+          const long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
+          // balanced base-256 digits: with u = v + 0x808080808080, the low six bytes of u are the
+          // digits d_1..d_6 (d in [-128, 127]) offset by 128, and u >> 48 is the top digit d_0
+          // (|d_0| <= 65). Offsets are removed below by flipping each byte's top bit.
+          const unsigned long long u = (unsigned long long)(v + 0x808080808080LL);
+          const uint32_t lo = (uint32_t)u, hi = (uint32_t)(u >> 32);
+          const uint32_t sh = 8 * r;
+          w[6] |= (lo & 0xffu) << sh;
+          w[5] |= ((lo >> 8) & 0xffu) << sh;
+          w[4] |= ((lo >> 16) & 0xffu) << sh;
+          w[3] |= (lo >> 24) << sh;
+          w[2] |= (hi & 0xffu) << sh;
+          w[1] |= ((hi >> 8) & 0xffu) << sh;
+          w[0] |= ((uint32_t)((int)hi >> 16) & 0xffu) << sh;
         }
+#pragma unroll
+        for (int p = 1; p < OZ_S; ++p) w[p] ^= 0x80808080u;
       }
 #pragma unroll
       for (int p = 0; p < OZ_S; ++p) dig[p][ii][kq] = w[p];
@@ -234,6 +243,16 @@ RP_DEVINL void oz_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+RP_DEVINL void oz_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
 // Lower 128 x 128 tiles (I, J <= I) of one matrix: I(I+1)/2 before row I.
 RP_DEVINL void oz_tile(int lin, int per, int& b, int& I, int& J) {
   b = lin / per;
@@ -272,7 +291,7 @@ struct OzArgs {
 // traffic from L2. The upper tile of a pair on the diagonal (J = I + 1) is computed but not
 // stored.
 template <int CL>
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
     oz_syrk_kernel(const __grid_constant__ CUtensorMap tm, OzArgs a) {
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -306,7 +325,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[s], CL);  // CL == 2: released by both CTAs' MMAs
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 8);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -389,9 +408,14 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5: TMEM lane quarter = warp % 4) ----------------
+    // ---------------- epilogue (warps 2..9: TMEM lane quarter = warp % 4, column half) ----------------
+    // Both passes of a tile are drained from TMEM into FP64 registers (64 columns per thread) and
+    // the accumulators released right away, so the MMAs of the next pass / tile start at once; the
+    // tile is then added into C with a single read-modify-write that overlaps those MMAs.
     const int quarter = warp & 3;
+    const int chalf = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
     int item = 0;
     for (int u = unit0; u < a.total_tiles; u += ustep) {
       int b, I, J;
@@ -399,53 +423,56 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int i = I * OZ_BM + row_in_tile;
       const int* Eb = a.E + (int64_t)b * a.M;
       const int ei = Eb[i];
-      double* Cb = a.C + (int64_t)b * a.cstride;
-      bool first_item = !a.subtract;
+      double acc[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
       for (int pass = 1; pass >= 0; --pass) {
         const int g0 = pass * OZ_GP;
         for (int ch = 0; ch < nchunks; ++ch, ++item) {
           mbar_wait(tfull, item & 1);
           oz_fence_after();
-#pragma unroll 1
-          for (int h = 0; h < 4; ++h) {
-            double part[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) part[c] = 0.0;
-#pragma unroll 1
-            for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
-              if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
-              uint32_t v[32];
-              oz_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g * 128 + h * 32), v);
-              const double w = ldexp(1.0, -8 * (g0 + g) - 12);
+          for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
+            if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
+            const double w = ldexp(1.0, -8 * (g0 + g) - 12);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) part[c] = fma((double)(int)v[c], w, part[c]);
-            }
-            // read-modify-write of this 32-column chunk: every load is issued before any store
-            // (a store could alias a later load otherwise and serialise 32 global round trips)
-            if (!valid) continue;  // the upper tile of a diagonal pair: accumulators drained only
-            double* dst0 = Cb + (int64_t)(J * OZ_BM + h * 32) * a.ldc + i;
-            double old[32];
-            if (!first_item) {
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t v[16];
+              oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), v);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) old[c] = __ldcg(dst0 + (int64_t)c * a.ldc);
-            }
-#pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int ej = Eb[J * OZ_BM + h * 32 + c];
-              double v;
-              if (ei == OZ_NONFINITE || ej == OZ_NONFINITE) {
-                v = __longlong_as_double(0x7ff8000000000000LL);
-              } else {
-                v = ldexp(part[c], ei + ej);
-                if (!first_item) v = a.subtract ? old[c] - v : old[c] + v;
-              }
-              dst0[(int64_t)c * a.ldc] = v;
+              for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)v[c], w, acc[q4 * 16 + c]);
             }
           }
-          first_item = false;
           oz_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty);
+        }
+      }
+      if (!valid) continue;  // the upper tile of a diagonal pair: accumulators drained only
+#ifdef OZ_DBG_NOSTORE
+      if (acc[0] != 12345.0) continue;  // experiments: TMEM drain without the C read-modify-write
+#endif
+      double* dst0 = a.C + (int64_t)b * a.cstride + (int64_t)(J * OZ_BM + chalf * 64) * a.ldc + i;
+      const int* Ej = Eb + J * OZ_BM + chalf * 64;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        // every load of a 16-column group is issued before its stores
+        double old[16];
+        if (a.subtract) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) old[c] = __ldcg(dst0 + (int64_t)(q4 * 16 + c) * a.ldc);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int ej = Ej[q4 * 16 + c];
+          double v;
+          if (ei == OZ_NONFINITE || ej == OZ_NONFINITE) {
+            v = __longlong_as_double(0x7ff8000000000000LL);
+          } else {
+            v = ldexp(acc[q4 * 16 + c], ei + ej);
+            if (a.subtract) v = old[c] - v;
+          }
+          dst0[(int64_t)(q4 * 16 + c) * a.ldc] = v;
         }
       }
     }
@@ -555,7 +582,7 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(OZ_THREADS);
+    cfg.blockDim = dim3(OZ_SYRK_THREADS);
     cfg.dynamicSmemBytes = OZ_SMEM;
     cfg.stream = st;
     cfg.attrs = attr;
@@ -578,7 +605,7 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   cudaFuncSetAttribute(oz_syrk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
   {
     ProfScope prof(prof_name, st);
-    oz_syrk_kernel<1><<<grid, OZ_THREADS, OZ_SMEM, st>>>(tm, a);
+    oz_syrk_kernel<1><<<grid, OZ_SYRK_THREADS, OZ_SMEM, st>>>(tm, a);
   }
   RP_LAUNCH_CHECK("ozaki syrk");
   return RP_OK;

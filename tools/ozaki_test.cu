@@ -22,7 +22,7 @@ int set_error(int code, const char* fmt, ...) {
 void count_launch() {}
 bool prof_on() { return false; }
 cudaEvent_t prof_event() { return nullptr; }
-void prof_push(const char*, cudaEvent_t, cudaEvent_t) {}
+void prof_push(const char*, cudaEvent_t, cudaEvent_t, cudaStream_t) {}
 }  // namespace rp
 
 static int run(int nblocks, int rows, int d, bool full_check, int reps) {
@@ -160,7 +160,49 @@ static void peak(int sms) {
   cudaFree(out);
 }
 
+// Trailing-update shapes of the blocked Cholesky: C_b -= A_b A_b^T with A_b = the M x K panel
+// below the diagonal inside a d x d column-major matrix (lda = d), nbatch matrices.
+static void trailing(int d, int M, int K, int nbatch, int reps) {
+  double *dA, *dC;
+  const size_t nn = (size_t)nbatch * d * d;
+  cudaMalloc(&dA, nn * 8);
+  cudaMalloc(&dC, nn * 8);
+  std::vector<double> h((size_t)d * d);
+  std::mt19937_64 gen(7);
+  std::normal_distribution<double> nd(0.0, 1.0);
+  for (auto& v : h) v = nd(gen);
+  for (int b = 0; b < nbatch; ++b) cudaMemcpy(dA + (size_t)b * d * d, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
+  cudaMemset(dC, 0, nn * 8);
+  const rp::OzIn in{dA + (d - M), d, (int64_t)d * d, K, M, nbatch};
+  void* work;
+  cudaMalloc(&work, rp::oz_workspace_bytes(M, K, nbatch));
+  double* C = dC + (size_t)(d - M) * d + (d - M);
+  rp::oz_syrk(in, C, d, (int64_t)d * d, true, work, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) rp::oz_syrk(in, C, d, (int64_t)d * d, true, work, 0);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  ms /= reps;
+  const double flops = (double)nbatch * M * (M + 128.0) * K;  // lower 128-tiles incl. diagonal tiles
+  printf("trailing M=%d K=%d batch=%d: %.3f ms, %.1f FP64-equivalent TFLOP/s (%s)\n", M, K, nbatch, ms,
+         flops / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(dA);
+  cudaFree(dC);
+  cudaFree(work);
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 't') {
+    const int shapes[][3] = {{2560, 1536, 10}, {1024, 1536, 10}, {2560, 1536, 40}, {3072, 1024, 10},
+                             {3584, 512, 10}, {3584, 512, 40}, {2048, 2048, 10}, {3328, 768, 10}};
+    for (auto& sh : shapes) trailing(4096, sh[0], sh[1], sh[2], 5);
+    return 0;
+  }
   if (argc > 1 && argv[1][0] == 'p') {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
