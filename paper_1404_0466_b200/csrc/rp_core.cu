@@ -1113,14 +1113,14 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
   const size_t base =
       (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + (int64_t)nf * N) + 1023) / 1024 * 1024;
   if (g_holdout_ozaki && oz_holdout_supported(d, N, nf) && ((uintptr_t)work & 15) == 0) {
-    // w^T G w = 2 w^T T w on the int8 tensor cores: partials [f][2 * mtiles][N]
+    // w^T G w = 2 w^T T w on the int8 tensor cores: partials [f][mtiles][N]
     int rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial,
                         reinterpret_cast<uint8_t*>(work) + base, st);
     if (rc) return rc;
     holdout_bc_kernel<<<dim3((N + 31) / 32, nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
     RP_LAUNCH_CHECK("holdout bc");
-    holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, 2 * mtiles, N, m, n_val, RP_METRIC_RMSE,
-                                                               yy, bc, 2.0, curves);
+    holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy,
+                                                               bc, 2.0, curves);
     RP_LAUNCH_CHECK("holdout gram finish");
     return RP_OK;
   }

@@ -37,11 +37,10 @@ namespace rp {
 
 constexpr int OZ_S = 7;  // slices: balanced base-256 digits of a 54-bit fixed-point value
 constexpr int OZ_BM = 128, OZ_BK = 32, OZ_STAGES = 3, OZ_GP = 4;
-constexpr int OZ_THREADS = 192;       // hold-out kernel: producer, MMA, 4 epilogue warps
-constexpr int OZ_SYRK_THREADS = 320;  // SYRK kernel: producer, MMA, 8 epilogue warps
+constexpr int OZ_SYRK_THREADS = 320;  // producer, MMA, 8 epilogue warps (SYRK and hold-out kernels)
 constexpr int OZ_SLICE = OZ_BM * OZ_BK;             // bytes of one 128 x 32 slice tile
 constexpr int OZ_STAGE = 2 * OZ_S * OZ_SLICE;        // A_I and A_J, all slices
-constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 128 + 4 * 32 * 8;
+constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 128 + 4 * 128 * 8;  // + hold-out row reduction
 // Row exponent marking a row with a NaN or infinity: the entries it touches are NaN, as in FP64.
 constexpr int OZ_NONFINITE = 0x7fffffff;
 
@@ -617,8 +616,9 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
 // T_b W_b at a time, K = rows k < 128(I+1) only (T is lower triangular); A = slices of T_b
 // (shared by all b when the batch stride of G is 0), B = slices of W_b^T. The epilogue scales
 // the tile to FP64, multiplies by W_b(i, n), reduces over the 128 rows (warp reduce-scatter,
-// then the 4 epilogue warps through shared memory) and writes one partial per (tile row, pass):
-// part[b][2 * I + pass][n], summed in a fixed order by the finish kernel.
+// then the 4 row quarters through shared memory) and writes one partial per tile row:
+// part[b][I][n], summed in a fixed order by the finish kernel. As in the SYRK, 8 epilogue warps
+// drain both passes of a tile into FP64 registers and release TMEM before the reduction.
 struct OzDotArgs {
   const int* EA;  // [nA][MpadA]
   const int* EB;  // [nbatch][MpadB]
@@ -629,7 +629,7 @@ struct OzDotArgs {
   int64_t kpad;
 };
 
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
     oz_dotb_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzDotArgs a) {
   extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -638,7 +638,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
   uint64_t* tfull = empty + OZ_STAGES;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* red = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE + 128);  // [4][32]
+  double* red = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE + 128);  // [4][128]
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int per_I = a.nbatch * a.ntB;
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 8);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -729,8 +729,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       }
     }
   } else {
-    const int quarter = warp & 3;
+    // epilogue warps 2..9: TMEM lane quarter = warp % 4, 64-column half = (warp - 2) / 4
+    const int quarter = warp & 3, chalf = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
     int item = 0;
     for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
       int b, I, J;
@@ -740,62 +742,67 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
       const int ei = a.EA[(int64_t)ba * a.MpadA + i];
       const int* EBb = a.EB + (int64_t)b * a.MpadB;
       const double* Wrow = a.W + (int64_t)b * a.w_stride + (int64_t)i * a.ldw;
+      double acc[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
       for (int pass = 1; pass >= 0; --pass, ++item) {
         const int g0 = pass * OZ_GP;
         mbar_wait(tfull, item & 1);
         oz_fence_after();
-#pragma unroll 1
-        for (int h = 0; h < 4; ++h) {
-          double v[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) v[c] = 0.0;
-#pragma unroll 1
-          for (int g = OZ_GP - 1; g >= 0; --g) {
-            if (g0 + g >= OZ_S) continue;  // groups past S - 1 are not computed
-            uint32_t t[32];
-            oz_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(g * 128 + h * 32), t);
-            const double w = ldexp(1.0, -8 * (g0 + g) - 12);
+        for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
+          if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
+          const double w = ldexp(1.0, -8 * (g0 + g) - 12);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = fma((double)(int)t[c], w, v[c]);
-          }
-          const int n0 = J * OZ_BM + h * 32;
-          if (h == 3) {  // the accumulators are no longer needed: let the next pass start
-            oz_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty);
-          }
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t t[16];
+            oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), t);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const int n = n0 + c;
-            const int en = EBb[n];
-            double x = 0.0;
-            if (i < a.d && n < a.N) {
-              x = (ei == OZ_NONFINITE || en == OZ_NONFINITE) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                              : ldexp(v[c], ei + en) * Wrow[n];
-            }
-            v[c] = x;
+            for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)t[c], w, acc[q4 * 16 + c]);
           }
-          // reduce-scatter over the warp's 32 rows: lane L ends with column n0 + L
+        }
+        oz_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty);  // the next pass / tile may overwrite the accumulators
+      }
+      const int n0 = J * OZ_BM + chalf * 64;
 #pragma unroll
-          for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-            const bool upper = (lane & s2) != 0;
+      for (int c = 0; c < 64; ++c) {
+        const int n = n0 + c;
+        double x = 0.0;
+        if (i < a.d && n < a.N) {
+          const int en = EBb[n];
+          x = (ei == OZ_NONFINITE || en == OZ_NONFINITE) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                          : ldexp(acc[c], ei + en) * Wrow[n];
+        }
+        acc[c] = x;
+      }
+      // reduce-scatter over the warp's 32 rows, per 32 columns: lane L ends with column n0 + 32 hh + L
 #pragma unroll
-            for (int j = 0; j < s2; ++j) {
-              const double send = upper ? v[j] : v[j + s2];
-              const double keep = upper ? v[j + s2] : v[j];
-              v[j] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
-            }
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+          const bool upper = (lane & s2) != 0;
+#pragma unroll
+          for (int j = 0; j < s2; ++j) {
+            const double send = upper ? acc[hh * 32 + j] : acc[hh * 32 + j + s2];
+            const double keep = upper ? acc[hh * 32 + j + s2] : acc[hh * 32 + j];
+            acc[hh * 32 + j] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
           }
-          red[quarter * 32 + lane] = v[0];
-          named_bar_sync(1, 128);
-          if (quarter == 0) {
-            const double tot = red[lane] + red[32 + lane] + red[64 + lane] + red[96 + lane];
-            const int n = n0 + lane;
-            if (n < a.N) a.part[(((int64_t)b * a.mtA + I) * 2 + pass) * a.N + n] = tot;
-          }
-          named_bar_sync(1, 128);
+        }
+        red[quarter * 128 + chalf * 64 + hh * 32 + lane] = acc[hh * 32];
+      }
+      named_bar_sync(1, 256);
+      if (quarter == 0) {  // rows summed in quarter order
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int col = chalf * 64 + hh * 32 + lane;
+          const double tot = red[col] + red[128 + col] + red[256 + col] + red[384 + col];
+          const int n = J * OZ_BM + col;
+          if (n < a.N) a.part[((int64_t)b * a.mtA + I) * a.N + n] = tot;
         }
       }
+      named_bar_sync(1, 256);
     }
   }
   __syncthreads();
@@ -818,7 +825,7 @@ inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
          oz_encode_fn() != nullptr;
 }
 
-// part[b][2 * I + pass][n]: partials of w_n^T T_b w_n (sum over the 2 * ceil(d/128) entries).
+// part[b][I][n]: partials of w_n^T T_b w_n (sum over the ceil(d/128) entries).
 inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
                       int64_t N, int nbatch, double* part, void* work, cudaStream_t st) {
   const bool shared = g_stride == 0;
@@ -867,7 +874,7 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
   {
     ProfScope prof("oz_holdout", st);
-    oz_dotb_kernel<<<grid, OZ_THREADS, OZ_SMEM, st>>>(ta, tb, a);
+    oz_dotb_kernel<<<grid, OZ_SYRK_THREADS, OZ_SMEM, st>>>(ta, tb, a);
   }
   RP_LAUNCH_CHECK("ozaki holdout");
   return RP_OK;
