@@ -193,6 +193,55 @@ RP_DEVINL void oz_commit(uint64_t* bar) {
                : "memory");
 }
 
+// All products S_p S_q^T of one K-step whose weight group g = p + q lies in [G0, G0 + OZ_GP), into
+// accumulator slab g - G0. G0 is a compile-time constant so the (p, q) list is fully unrolled
+// with constant descriptor offsets, and the issuing warp runs converged so the operands stay in
+// uniform registers; one elected lane issues each MMA (the issue loop, not the tensor pipe, bounded
+// the kernel while one thread rebuilt the descriptors and branched per MMA: c4 Gram 23.4 -> 19.6
+// ms). BSL: bytes between consecutive B slices in shared memory. Call with the whole warp.
+template <int G0, int BSL, bool PAIR>
+RP_DEVINL void oz_issue_kstep(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_t first) {
+#pragma unroll
+  for (int p = 0; p < OZ_S; ++p)
+#pragma unroll
+    for (int q = 0; q < OZ_S - p; ++q) {
+      if (p + q < G0 || p + q >= G0 + OZ_GP) continue;
+      const uint64_t da = da0 + (uint64_t)(p * (OZ_SLICE >> 4));
+      const uint64_t db = db0 + (uint64_t)(q * (BSL >> 4));
+      const uint32_t acc = (p == 0) ? (first ? 0u : 1u) : 1u;  // p = 0 starts every group of the pass
+      const uint32_t d = tmem + (uint32_t)((p + q - G0) * 128);
+      if (PAIR)  // issued by the whole (converged) warp: operands stay warp-uniform, one elected lane issues
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+            "l"(da), "l"(db), "r"((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                                  ((uint32_t)(256 >> 4) << 24)),
+            "r"(acc));
+      else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+            "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
+    }
+}
+
+// Whole-warp variants (the MMA issuer warp runs its loop converged; one elected lane commits).
+RP_DEVINL void oz_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+RP_DEVINL void oz_commit_mc_warp(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 RP_DEVINL void oz_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 RP_DEVINL void oz_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -276,10 +325,12 @@ RP_DEVINL void oz_pair(int lin, int per, int& b, int& I, int& jp) {
 }
 
 struct OzArgs {
-  const int* E;      // [nbatch][M]
+  const int* E;      // [nbatch][Mp]
   double* C;         // C_b at C + b * cstride, column-major, leading dimension ldc
   int64_t ldc, cstride;
   int M, per, total_tiles;
+  int Mp = 0;        // rows per (batch, slice) of the slice layout (pair kernel: M rounded up to 256)
+  int dbg = 0;       // experiments (RP_OZAKI_DBG, pair kernel): 1 = no operand loads, 2 = no MMAs
   int subtract;      // 0: C = A A^T, 1: C -= A A^T
   int64_t kpad, kchunk;
 };
@@ -345,7 +396,7 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
         int b, I, J;
         unit_tile(u, b, I, J);
         const int Jl = J < mt ? J : I;  // past the last column tile: load a valid (unused) tile
-        const int rowA = b * OZ_S * a.M + I * OZ_BM, rowB = b * OZ_S * a.M + Jl * OZ_BM;
+        const int rowA = b * OZ_S * a.Mp + I * OZ_BM, rowB = b * OZ_S * a.Mp + Jl * OZ_BM;
         for (int pass = 1; pass >= 0; --pass) {
           const int ns = pass ? OZ_S : OZ_GP;  // slices the pass reads
           const int half = (ns + 1) / 2;
@@ -358,18 +409,18 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
             uint8_t* sb = sa + OZ_S * OZ_SLICE;
             for (int p = pa0; p < pa1; ++p) {
               if (CL == 2)
-                oz_tma_2d_mc(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.M, &full[st], (uint16_t)3);
+                oz_tma_2d_mc(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.Mp, &full[st], (uint16_t)3);
               else
-                oz_tma_2d(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.M, &full[st]);
+                oz_tma_2d(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.Mp, &full[st]);
             }
-            for (int p = 0; p < ns; ++p) oz_tma_2d(sb + p * OZ_SLICE, &tm, (int)k, rowB + p * a.M, &full[st]);
+            for (int p = 0; p < ns; ++p) oz_tma_2d(sb + p * OZ_SLICE, &tm, (int)k, rowB + p * a.Mp, &full[st]);
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer (the whole warp runs the loop, one elected lane issues) ----------------
+    {
       int it = 0, item = 0;
       for (int u = unit0; u < a.total_tiles; u += ustep) {
         for (int pass = 1; pass >= 0; --pass) {
@@ -385,23 +436,17 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
               const uint32_t sa = smem_u32(smem + st * OZ_STAGE);
               const uint32_t sb = sa + OZ_S * OZ_SLICE;
               const bool first = (k == kb);
-#pragma unroll
-              for (int p = 0; p < OZ_S; ++p)
-#pragma unroll
-                for (int q = 0; q < OZ_S - p; ++q) {
-                  const int g = p + q;
-                  if (g < g0 || g >= g0 + OZ_GP) continue;
-                  // p = 0 touches every group of the pass first (q = g): it starts the group
-                  oz_mma(tmem + (uint32_t)((g - g0) * 128), oz_desc_sw32(sa + p * OZ_SLICE),
-                         oz_desc_sw32(sb + q * OZ_SLICE), (first && p == 0) ? 0u : 1u);
-                }
+              if (g0)
+                oz_issue_kstep<OZ_GP, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
+              else
+                oz_issue_kstep<0, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
               // frees the stage (in both CTAs of a pair) once these MMAs have read it
               if (CL == 2)
-                oz_commit_mc(&empty[st], (uint16_t)3);
+                oz_commit_mc_warp(&empty[st], (uint16_t)3);
               else
-                oz_commit(&empty[st]);
+                oz_commit_warp(&empty[st]);
             }
-            oz_commit(tfull);
+            oz_commit_warp(tfull);
           }
         }
       }
@@ -420,7 +465,7 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
       int b, I, J;
       const bool valid = unit_tile(u, b, I, J);
       const int i = I * OZ_BM + row_in_tile;
-      const int* Eb = a.E + (int64_t)b * a.M;
+      const int* Eb = a.E + (int64_t)b * a.Mp;
       const int ei = Eb[i];
       double acc[64];
 #pragma unroll
@@ -481,6 +526,256 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+// ------------------------------------------------------------------ CTA-pair (cta_group::2) SYRK
+// A 2-CTA cluster computes a 256 x 128 block (sub-tile rows 2 I2 and 2 I2 + 1, column tile J) with
+// tcgen05.mma.cta_group::2 (M = 256, N = 128, K = 32): each CTA stages its own 128 rows of A and
+// half (64 rows) of B_J, so per SM the tensor core reads 6 KB of shared memory per 128 x 128 x 32
+// product instead of 8 KB and the TMA writes 25% fewer operand bytes -- the single-CTA kernel is
+// bound by shared-memory bandwidth, not by L2 (a 4th stage changed nothing). The leader CTA
+// (rank 0) issues the MMAs; both CTAs' TMA loads complete on the leader's full barrier
+// (.cta_group::2), the MMA commits are multicast to both CTAs' empty / tfull barriers, and both
+// CTAs' epilogue warps release the accumulators on the leader's tempty barrier. Each CTA drains
+// and stores its own 128 x 128 sub-tile exactly as the single-CTA epilogue does.
+
+constexpr uint32_t OZ_IDESC_PAIR = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
+                                   ((uint32_t)(256 >> 4) << 24);
+
+RP_DEVINL uint32_t oz_mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+RP_DEVINL void oz_mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAITC_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+RP_DEVINL void oz_mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+
+RP_DEVINL void oz_tma_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+RP_DEVINL void oz_mma_pair(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(OZ_IDESC_PAIR), "r"(accumulate));
+}
+
+// (whole warp; one elected lane commits)
+RP_DEVINL void oz_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+constexpr int OZ_PSLICE_B = 64 * OZ_BK;                     // bytes of one 64 x 32 B-half slice tile
+constexpr int OZ_PSTAGE = OZ_S * (OZ_SLICE + OZ_PSLICE_B);  // A (128 rows) and B half (64 rows), all slices
+constexpr int OZ_PSTAGES = 4;
+constexpr size_t OZ_PSMEM = 1024 + (size_t)OZ_PSTAGES * OZ_PSTAGE + 128;
+
+// Pair units of one matrix: sub-tile-row pair I2 (rows 2 I2, 2 I2 + 1), column tiles J <= 2 I2 + 1
+// (J < mt): 2 I2 + 2 units per full pair row, I2^2 + I2 before row I2.
+RP_DEVINL void oz_pair_unit(int lin, int per, int mt, int& b, int& I2, int& J) {
+  b = lin / per;
+  const int t = lin - b * per;
+  int i = (int)((sqrt(4.0 * t + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) <= t) ++i;
+  while (i * (i + 1) > t) --i;
+  I2 = i;
+  J = t - i * (i + 1);
+  (void)mt;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
+    oz_syrk_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs a) {
+  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_PSTAGES * OZ_PSTAGE);
+  uint64_t* empty = full + OZ_PSTAGES;
+  uint64_t* tfull = empty + OZ_PSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = oz_cluster_rank();
+  const int nchunks = (int)((a.kpad + a.kchunk - 1) / a.kchunk);
+  const int unit0 = blockIdx.x / 2, ustep = gridDim.x / 2;
+  const int mt = a.M / OZ_BM;  // sub-tile rows that exist (rows of the padded pair past mt are zero)
+
+  if (tid == 0) {
+    for (int s = 0; s < OZ_PSTAGES; ++s) {
+      mbar_init(&full[s], 1);   // leader: its producer's arrive + both CTAs' bytes
+      mbar_init(&empty[s], 1);  // the leader's MMA commit (multicast)
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);  // 8 epilogue warps of each CTA (used on the leader)
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_cluster_sync();
+  oz_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_leader = oz_mapa(smem_u32(full), 0);
+  const uint32_t tempty_leader = oz_mapa(smem_u32(tempty), 0);
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, own half of B) ----------------
+    if (lane == 0) {
+      int it = 0;
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
+        int b, I2, J;
+        oz_pair_unit(u, a.per, mt, b, I2, J);
+        const int rowA = b * OZ_S * a.Mp + (2 * I2 + (int)rank) * OZ_BM;
+        const int rowB = b * OZ_S * a.Mp + J * OZ_BM + (int)rank * 64;
+        for (int pass = 1; pass >= 0; --pass) {
+          const int ns = pass ? OZ_S : OZ_GP;
+          for (int64_t k = 0; k < a.kpad; k += OZ_BK, ++it) {
+            const int st = it % OZ_PSTAGES;
+            oz_mbar_wait_cluster(&empty[st], ((it / OZ_PSTAGES) & 1) ^ 1);
+            if (a.dbg & 1) {
+              if (rank == 0) mbar_arrive(&full[st]);
+              continue;
+            }
+            if (rank == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * (OZ_SLICE + OZ_PSLICE_B)));
+            uint8_t* sa = smem + st * OZ_PSTAGE;
+            uint8_t* sb = sa + OZ_S * OZ_SLICE;
+            const uint32_t fb = full_leader + (uint32_t)(st * 8);
+            for (int p = 0; p < ns; ++p) {
+              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, (int)k, rowA + p * a.Mp, fb);
+              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, (int)k, rowB + p * a.Mp, fb);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only; the whole warp runs the loop, one lane issues) ----------------
+    if (rank == 0) {
+      int it = 0, item = 0;
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
+        for (int pass = 1; pass >= 0; --pass) {
+          const int g0 = pass * OZ_GP;
+          for (int ch = 0; ch < nchunks; ++ch, ++item) {
+            oz_mbar_wait_cluster(tempty, (item & 1) ^ 1);  // both CTAs have drained the accumulators
+            oz_fence_after();
+            const int64_t kb = ch * a.kchunk, ke = (kb + a.kchunk < a.kpad) ? kb + a.kchunk : a.kpad;
+            for (int64_t k = kb; k < ke; k += OZ_BK, ++it) {
+              const int st = it % OZ_PSTAGES;
+              oz_mbar_wait_cluster(&full[st], (it / OZ_PSTAGES) & 1);
+              oz_fence_after();
+              const uint32_t sa = smem_u32(smem + st * OZ_PSTAGE);
+              const uint32_t sb = sa + OZ_S * OZ_SLICE;
+              const bool first = (k == kb);
+              if (a.dbg & 2) {
+              } else if (g0) {
+                oz_issue_kstep<OZ_GP, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
+              } else {
+                oz_issue_kstep<0, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
+              }
+              oz_commit_pair(&empty[st]);  // frees the stage in both CTAs once the MMAs have read it
+            }
+            oz_commit_pair(tfull);
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..9 of both CTAs): this CTA's 128-row sub-tile ----------------
+    const int quarter = warp & 3;
+    const int chalf = (warp - 2) >> 2;
+    const int row_in_tile = quarter * 32 + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
+    int item = 0;
+    for (int u = unit0; u < a.total_tiles; u += ustep) {
+      int b, I2, J;
+      oz_pair_unit(u, a.per, mt, b, I2, J);
+      const int I = 2 * I2 + (int)rank;
+      const bool valid = I < mt && J <= I;
+      const int i = I * OZ_BM + row_in_tile;
+      const int* Eb = a.E + (int64_t)b * a.Mp;
+      const int ei = valid ? Eb[i] : 0;
+      double acc[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+      for (int pass = 1; pass >= 0; --pass) {
+        const int g0 = pass * OZ_GP;
+        for (int ch = 0; ch < nchunks; ++ch, ++item) {
+          oz_mbar_wait_cluster(tfull, item & 1);
+          oz_fence_after();
+#pragma unroll
+          for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
+            if (g0 + g >= OZ_S) continue;
+            const double w = ldexp(1.0, -8 * (g0 + g) - 12);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint32_t v[16];
+              oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)v[c], w, acc[q4 * 16 + c]);
+            }
+          }
+          oz_fence_before();
+          __syncwarp();
+          if (lane == 0) oz_mbar_arrive_remote(tempty_leader);
+        }
+      }
+      if (!valid) continue;  // above the diagonal, or the zero rows past M
+      double* dst0 = a.C + (int64_t)b * a.cstride + (int64_t)(J * OZ_BM + chalf * 64) * a.ldc + i;
+      const int* Ej = Eb + J * OZ_BM + chalf * 64;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        double old[16];
+        if (a.subtract) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) old[c] = __ldcg(dst0 + (int64_t)(q4 * 16 + c) * a.ldc);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const int ej = Ej[q4 * 16 + c];
+          double v;
+          if (ei == OZ_NONFINITE || ej == OZ_NONFINITE) {
+            v = __longlong_as_double(0x7ff8000000000000LL);
+          } else {
+            v = ldexp(acc[q4 * 16 + c], ei + ej);
+            if (a.subtract) v = old[c] - v;
+          }
+          dst0[(int64_t)(q4 * 16 + c) * a.ldc] = v;
+        }
+      }
+    }
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_cluster_sync();  // no CTA deallocates or exits while its peer may still signal it
+  oz_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 // ------------------------------------------------------------------ host side
 
 inline PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
@@ -497,12 +792,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
 
 // 2-D int8 view of the slices: inner dim kpad bytes, outer nbatch*S*M rows; SWIZZLE_32B boxes of
 // 32 x 128.
-inline bool oz_tensor_map(CUtensorMap* m, const int8_t* slices, int64_t kpad, int64_t nrows) {
+inline bool oz_tensor_map(CUtensorMap* m, const int8_t* slices, int64_t kpad, int64_t nrows, int box_rows = OZ_BM) {
   auto enc = oz_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)nrows};
   cuuint64_t strides[1] = {(cuuint64_t)kpad};
-  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)OZ_BM};
+  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(slices), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -512,13 +807,17 @@ inline bool oz_tensor_map(CUtensorMap* m, const int8_t* slices, int64_t kpad, in
 
 inline size_t oz_eb(int M, int nbatch) { return ((size_t)nbatch * M * sizeof(int) + 1023) / 1024 * 1024; }
 
+// Rows of the SYRK slice layout: M rounded up to the 256-row blocks of the CTA-pair kernel.
+inline int oz_mp(int M) { return (M + 255) / 256 * 256; }
+
 inline size_t oz_workspace_bytes(int M, int64_t K, int nbatch) {
-  return oz_eb(M, nbatch) + (size_t)nbatch * OZ_S * M * (size_t)oz_kpad(K);
+  const int mp = oz_mp(M);
+  return oz_eb(mp, nbatch) + (size_t)nbatch * OZ_S * mp * (size_t)oz_kpad(K);
 }
 
 // Shapes the tensor-core path takes: 128-row tiles, int32 TMA coordinates.
 inline bool oz_supported(int M, int64_t K, int nbatch) {
-  return M % OZ_BM == 0 && (int64_t)nbatch * OZ_S * M < 0x7fffffff && oz_kpad(K) < 0x7fffffff &&
+  return M % OZ_BM == 0 && (int64_t)nbatch * OZ_S * oz_mp(M) < 0x7fffffff && oz_kpad(K) < 0x7fffffff &&
          oz_encode_fn() != nullptr;
 }
 
@@ -536,16 +835,24 @@ inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cuda
 // C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
 inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
                    cudaStream_t st, const char* prof_name = "oz_syrk") {
+  // RP_OZAKI_PAIR=0: independent CTAs (128 x 128 tiles) instead of CTA pairs (256 x 128 blocks)
+  static const bool pair = [] {
+    const char* e = getenv("RP_OZAKI_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  OzIn pin = in;
+  pin.Mpad = pair ? oz_mp(in.M) : in.M;
+  const int mp = pin.Mpad;
   int* E = reinterpret_cast<int*>(work);
-  int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(in.M, in.nbatch);
+  int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(mp, in.nbatch);
   const int64_t kpad = oz_kpad(in.K);
   {
     ProfScope prof("oz_prep", st);
-    int rc = oz_prepare(in, E, slices, kpad, st);
+    int rc = oz_prepare(pin, E, slices, kpad, st);
     if (rc) return rc;
   }
   CUtensorMap tm;
-  if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * in.M))
+  if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * mp))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
   OzArgs a;
   a.E = E;
@@ -553,6 +860,7 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   a.ldc = ldc;
   a.cstride = cstride;
   a.M = in.M;
+  a.Mp = mp;
   const int mt = in.M / OZ_BM;
   a.subtract = subtract ? 1 : 0;
   a.kpad = kpad;
@@ -560,10 +868,31 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // RP_OZAKI_CLUSTER=1: 2-CTA clusters sharing A_I by multicast. Halves the A traffic from L2
-  // but measured slower at c4 (Gram kernel 21.3 vs 20.1 ms: the pair runs in lockstep and
-  // wastes the diagonal pair's upper tile); the kernel is not L2-bound (a 4th stage also
-  // changed nothing), so the default is independent CTAs.
+  if (pair) {
+    CUtensorMap tmB;
+    if (!oz_tensor_map(&tmB, slices, kpad, (int64_t)in.nbatch * OZ_S * mp, 64))
+      return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
+    a.per = 0;
+    for (int i2 = 0; i2 < (mt + 1) / 2; ++i2) a.per += (2 * i2 + 2 < mt ? 2 * i2 + 2 : mt);
+    a.total_tiles = a.per * in.nbatch;  // pair units
+    static const int dbg = [] {
+      const char* e = getenv("RP_OZAKI_DBG");
+      return e ? atoi(e) : 0;
+    }();
+    a.dbg = dbg;
+    cudaFuncSetAttribute(oz_syrk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM);
+    int pairs = sms / 2;
+    if (pairs > a.total_tiles) pairs = a.total_tiles;
+    {
+      ProfScope prof(prof_name, st);
+      oz_syrk_pair_kernel<<<2 * pairs, OZ_SYRK_THREADS, OZ_PSMEM, st>>>(tm, tmB, a);
+    }
+    RP_LAUNCH_CHECK("ozaki syrk (CTA pairs)");
+    return RP_OK;
+  }
+  // RP_OZAKI_CLUSTER=1 (with RP_OZAKI_PAIR=0): 2-CTA clusters sharing A_I by multicast. Measured
+  // slower at c4 (Gram kernel 21.3 vs 20.1 ms: the pair runs in lockstep and wastes the diagonal
+  // pair's upper tile).
   static const bool cluster = [] {
     const char* e = getenv("RP_OZAKI_CLUSTER");
     return e && e[0] == '1';
@@ -697,7 +1026,7 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {  // the whole warp runs the loop, one elected lane issues
       int it = 0, item = 0;
       for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
         int b, I, J;
@@ -713,18 +1042,13 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
             oz_fence_after();
             const uint32_t sa = smem_u32(smem + st * OZ_STAGE);
             const uint32_t sb = sa + OZ_S * OZ_SLICE;
-#pragma unroll
-            for (int p = 0; p < OZ_S; ++p)
-#pragma unroll
-              for (int q = 0; q < OZ_S - p; ++q) {
-                const int g = p + q;
-                if (g < g0 || g >= g0 + OZ_GP) continue;
-                oz_mma(tmem + (uint32_t)((g - g0) * 128), oz_desc_sw32(sa + p * OZ_SLICE),
-                       oz_desc_sw32(sb + q * OZ_SLICE), (kk == 0 && p == 0) ? 0u : 1u);
-              }
-            oz_commit(&empty[st]);
+            if (g0)
+              oz_issue_kstep<OZ_GP, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
+            else
+              oz_issue_kstep<0, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
+            oz_commit_warp(&empty[st]);
           }
-          oz_commit(tfull);
+          oz_commit_warp(tfull);
         }
       }
     }
