@@ -542,80 +542,21 @@ __global__ void select_kernel(const double* curves, int k, int q, int m, double*
   }
 }
 
-// C_b = X_b^T Y_b for few outputs (m <= 16): a streaming FP64 kernel that reads X once. It is
-// sized to co-reside with the Gram SYRK (128 threads, <= 120 registers next to the SYRK's
-// 288 x 168) and is launched on a side stream, so it runs in the SYRK's shadow: the SYRK is
-// bound by the DMMA pipe at ~5% of HBM bandwidth, this kernel by HBM.
-// CTA = 128 columns of one block; 2 row groups of 64 threads, 2 adjacent columns per thread,
-// rows interleaved across the groups; the partials are combined in a fixed order.
-template <int MT>
-__global__ void __maxnreg__(120) xty_kernel(const double* X, int64_t ldx, int64_t rows, int d, const double* Y,
-                                                  int64_t ldy, int mrt, double* C) {
-  constexpr int MM = MT ? MT : 16;
-  constexpr int RG = 2;
-  const int m = MT ? MT : mrt;
-  __shared__ double red[RG - 1][128];
-  const int b = blockIdx.y, tx = threadIdx.x & 63, grp = threadIdx.x >> 6;
-  const int c = blockIdx.x * 128 + 2 * tx;
-  const double* Xb = X + (int64_t)b * rows * ldx;
-  const double* Yb = Y + (int64_t)b * rows * ldy;
-  double a0[MM], a1[MM];
-#pragma unroll
-  for (int o = 0; o < MM; ++o) a0[o] = a1[o] = 0.0;
-  if (c < d) {
-    const bool pair = c + 1 < d;
-#pragma unroll 4
-    for (int64_t r = grp; r < rows; r += RG) {
-      double x0, x1 = 0.0;
-      if (pair) {
-        const double2 v = __ldcs(reinterpret_cast<const double2*>(Xb + r * ldx + c));
-        x0 = v.x;
-        x1 = v.y;
-      } else {
-        x0 = __ldcs(Xb + r * ldx + c);
-      }
-      const double* yr = Yb + r * ldy;
-#pragma unroll
-      for (int o = 0; o < MM; ++o)
-        if (o < m) {
-          const double y = __ldg(yr + o);
-          a0[o] = fma(x0, y, a0[o]);
-          a1[o] = fma(x1, y, a1[o]);
-        }
-    }
-  }
-#pragma unroll
-  for (int o = 0; o < MM; ++o) {
-    if (o >= m) break;
-    if (grp > 0) {
-      red[grp - 1][2 * tx] = a0[o];
-      red[grp - 1][2 * tx + 1] = a1[o];
-    }
-    __syncthreads();
-    if (grp == 0 && c < d) {
-      double s0 = a0[o], s1 = a1[o];
-      for (int g2 = 0; g2 < RG - 1; ++g2) {
-        s0 += red[g2][2 * tx];
-        s1 += red[g2][2 * tx + 1];
-      }
-      C[((int64_t)b * m + o) * d + c] = s0;
-      if (c + 1 < d) C[((int64_t)b * m + o) * d + c + 1] = s1;
-    }
-    __syncthreads();
-  }
-}
-
-static int xty(const double* X, int64_t ldx, int64_t rows, int nblocks, int d, const double* Y, int64_t ldy, int m,
-               double* C, cudaStream_t st) {
-  dim3 grid((d + 127) / 128, nblocks);
+// C_b = X_b^T Y_b for few outputs (m <= 16), optionally with the Ozaki row exponents of X_b^T
+// (E != nullptr): oz_gram_prep_kernel, one pass over X. The FP64 (DMMA) Gram runs it on a side
+// stream without E, so C is bit-identical whichever Gram path is taken.
+static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, int d, const double* Y, int64_t ldy,
+                     int m, int* E, int mp, double* C, cudaStream_t st) {
+  dim3 grid(((E ? mp : d) + 31) / 32, nblocks);
   switch (m) {
-#define RP_XTY(M) \
-  case M: xty_kernel<M><<<grid, 128, 0, st>>>(X, ldx, rows, d, Y, ldy, m, C); break;
-    RP_XTY(1) RP_XTY(2) RP_XTY(4) RP_XTY(8) RP_XTY(10) RP_XTY(16)
-#undef RP_XTY
-    default: xty_kernel<0><<<grid, 128, 0, st>>>(X, ldx, rows, d, Y, ldy, m, C);
+#define RP_GPREP(M) \
+  case M: oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, mp, E, C); break;
+    RP_GPREP(1) RP_GPREP(2) RP_GPREP(3) RP_GPREP(4) RP_GPREP(5) RP_GPREP(6) RP_GPREP(7) RP_GPREP(8)
+    RP_GPREP(9) RP_GPREP(10) RP_GPREP(11) RP_GPREP(12) RP_GPREP(13) RP_GPREP(14) RP_GPREP(15) RP_GPREP(16)
+#undef RP_GPREP
+    default: return set_error(RP_EINVAL, "gram prep: m=%d outside [1, 16]", m);
   }
-  RP_LAUNCH_CHECK("gram xty");
+  RP_LAUNCH_CHECK("gram prep");
   return RP_OK;
 }
 
@@ -698,7 +639,9 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   a.lower_only = 1;
   const bool want_c = m > 0 && C != nullptr;
   if (want_c) RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
-  const bool side = want_c && m <= 16 && aligned16(X) && ldx % 2 == 0 && !g_xty_gemm;
+  // tensor-core path with C wanted: one fused pass computes the slicing exponents and X^T Y
+  const bool fused = ozaki && want_c && m <= 16 && !g_xty_gemm && oz_pair_enabled();
+  const bool side = !fused && want_c && m <= 16 && !g_xty_gemm;
   cudaStream_t xs = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   if (side) {
@@ -714,11 +657,20 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   }
   // X_b row-major (rows x d) is the column-major d x rows matrix A_b with lda = ldx: G_b = A_b A_b^T
   const OzIn oin{X, ldx, rows_per_block * ldx, rows_per_block, d, nblocks};
+  if (fused) {
+    // one pass over X for the row exponents of the slicing and C_b = X_b^T Y_b, then the SYRK
+    {
+      ProfScope prof("gram_prep", st);
+      int rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, reinterpret_cast<int*>(work), oz_mp(d), C, st);
+      if (rc) return rc;
+    }
+    return oz_syrk(oin, G, d, (int64_t)d * d, false, work, st, "oz_syrk", true);
+  }
   int rc = ozaki ? oz_syrk(oin, G, d, (int64_t)d * d, false, work, st)
                  : gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
   if (rc) return rc;
   if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
-    rc = xty(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, C, xs);
+    rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, nullptr, d, C, xs);
     if (rc) return rc;
     cudaEventRecord(join, xs);
     cudaStreamWaitEvent(st, join, 0);

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E) {
   smx[wk][lane] = mx;
   sfin[wk][lane] = finite ? 1 : 0;
   __syncthreads();
-  if (wk == 0 && i < mp) {
+  if (E != nullptr && wk == 0 && i < mp) {
     for (int w = 1; w < 8; ++w) {
       mx = fmax(mx, smx[w][lane]);
       finite = finite && sfin[w][lane];
@@ -96,6 +96,64 @@ __global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E) {
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);
     E[(int64_t)b * mp + i] = (i < in.M && !finite) ? OZ_NONFINITE : e;
+  }
+}
+
+// Gram blocks: the row exponents of A_b = X_b^T fused with C_b = X_b^T Y_b (both need one pass
+// over X_b; done separately they read X twice more than the slicing does). X_b row-major
+// (rows x d, leading dimension ldx), Y_b row-major (rows x m, ldy). One CTA per 32 columns of X_b:
+// 8 warps stride over the rows (lane = column: every row read is a coalesced 256-byte segment, the
+// Y row is a broadcast), then the max and the per-warp sums are combined in a fixed order.
+// E[b][i] as oz_rowexp_kernel (stride mp, rows i >= d get 0; E = nullptr: X^T Y only, the FP64
+// Gram's side stream); C[b][o][i] (column-major d x m). The same X^T Y summation order either way.
+template <int MT>
+__global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int64_t ldx, int64_t rows, int d,
+                                                           const double* Y, int64_t ldy, int m, int mp, int* E,
+                                                           double* C) {
+  constexpr int MM = MT > 0 ? MT : 1;
+  __shared__ double smx[8][32];
+  __shared__ int sfin[8][32];
+  __shared__ double ssum[8][MM][32];
+  const int b = blockIdx.y, lane = threadIdx.x & 31, wk = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  double mx = 0.0, acc[MM];
+#pragma unroll
+  for (int o = 0; o < MM; ++o) acc[o] = 0.0;
+  bool finite = true;
+  if (i < d) {
+    const double* x = X + (int64_t)b * rows * ldx + i;
+    const double* y = Y + (int64_t)b * rows * ldy;
+#pragma unroll 4
+    for (int64_t r = wk; r < rows; r += 8) {
+      const double xv = __ldcs(x + r * ldx);
+      const double v = fabs(xv);
+      finite &= (v <= 1.79769313486231570e308);
+      mx = fmax(mx, v);
+      const double* yr = y + r * ldy;
+#pragma unroll
+      for (int o = 0; o < MM; ++o) acc[o] = fma(xv, __ldg(yr + o), acc[o]);
+    }
+  }
+  smx[wk][lane] = mx;
+  sfin[wk][lane] = finite ? 1 : 0;
+#pragma unroll
+  for (int o = 0; o < MM; ++o) ssum[wk][o][lane] = acc[o];
+  __syncthreads();
+  if (E != nullptr && wk == 0 && i < mp) {
+    for (int w = 1; w < 8; ++w) {
+      mx = fmax(mx, smx[w][lane]);
+      finite = finite && sfin[w][lane];
+    }
+    int e = 0;
+    if (mx > 0.0) frexp(mx, &e);
+    E[(int64_t)b * mp + i] = (i < d && !finite) ? OZ_NONFINITE : e;
+  }
+  if (i < d) {
+    for (int o = wk; o < m; o += 8) {
+      double sacc = 0.0;
+      for (int w = 0; w < 8; ++w) sacc += ssum[w][o][lane];
+      C[((int64_t)b * m + o) * d + i] = sacc;
+    }
   }
 }
 
@@ -833,13 +891,20 @@ inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cuda
 }
 
 // C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
-inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
-                   cudaStream_t st, const char* prof_name = "oz_syrk") {
-  // RP_OZAKI_PAIR=0: independent CTAs (128 x 128 tiles) instead of CTA pairs (256 x 128 blocks)
+// exps_ready: the row exponents are already in the workspace (E[b * oz_mp(M) + i], e.g. from
+// oz_gram_prep_kernel), so only the slicing pass runs.
+// RP_OZAKI_PAIR=0: independent CTAs (128 x 128 tiles) instead of CTA pairs (256 x 128 blocks)
+inline bool oz_pair_enabled() {
   static const bool pair = [] {
     const char* e = getenv("RP_OZAKI_PAIR");
     return !(e && e[0] == '0');
   }();
+  return pair;
+}
+
+inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
+                   cudaStream_t st, const char* prof_name = "oz_syrk", bool exps_ready = false) {
+  const bool pair = oz_pair_enabled();
   OzIn pin = in;
   pin.Mpad = pair ? oz_mp(in.M) : in.M;
   const int mp = pin.Mpad;
@@ -848,8 +913,14 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   const int64_t kpad = oz_kpad(in.K);
   {
     ProfScope prof("oz_prep", st);
-    int rc = oz_prepare(pin, E, slices, kpad, st);
-    if (rc) return rc;
+    if (exps_ready && pair) {
+      oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(pin, E, slices,
+                                                                                                      kpad);
+      RP_LAUNCH_CHECK("ozaki slice");
+    } else {
+      int rc = oz_prepare(pin, E, slices, kpad, st);
+      if (rc) return rc;
+    }
   }
   CUtensorMap tm;
   if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * mp))
