@@ -61,7 +61,7 @@ int64_t rp_theta_size(int d, int r);
 
 /* (1) Hessian blocks.  Replaces ridge.assemble (ridge.py:50-60): H = X^T X
  * (:58-59) and g = X^T y (:60), evaluated per contiguous row block so that
- * H_f = sum_b G_b - G_f (folds.py contiguous FoldPlan, cvsearch.py:145-147).
+ * H_f = sum_{b != f} G_b (contiguous FoldPlan, cvsearch.py:145-147).
  *   X: nblocks * rows_per_block rows, row-major, leading dim ldx (>= d)
  *   Y: same rows, row-major (rows x m), leading dim ldy (>= m); may be NULL when m == 0
  *   G: nblocks x (d x d column-major); the lower triangle is written (and the
@@ -69,9 +69,10 @@ int64_t rp_theta_size(int d, int r);
  *   C: nblocks x (d x m column-major)  (X_b^T Y_b)
  *   work: rp_gram_workspace_size(d, rows_per_block, nblocks) bytes (16-byte
  *      aligned), or NULL. With a workspace and d % 128 == 0, G is computed on
- *      the int8 tensor cores (tcgen05) by the Ozaki scheme with 8 seven-bit
- *      slices per value -- FP64-level accuracy (~1e-15 relative to
- *      sqrt(G_ii G_jj)), NaN/inf propagated; otherwise by FP64 DMMA.   */
+ *      the int8 tensor cores (tcgen05, CTA pairs) by the Ozaki scheme with 7
+ *      balanced base-256 digits per value -- FP64-level accuracy (~1e-15
+ *      relative to sqrt(G_ii G_jj)), NaN/inf propagated; otherwise by FP64
+ *      DMMA. C is computed by the same FP64 kernel on either path.   */
 size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks);
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d,
                    const double* Y, int64_t ldy, int m, double* G, double* C, void* work, void* stream);
