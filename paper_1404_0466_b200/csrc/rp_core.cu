@@ -544,19 +544,34 @@ __global__ void select_kernel(const double* curves, int k, int q, int m, double*
 
 // C_b = X_b^T Y_b for few outputs (m <= 16), optionally with the Ozaki row exponents of X_b^T
 // (E != nullptr): oz_gram_prep_kernel, one pass over X. The FP64 (DMMA) Gram runs it on a side
-// stream without E, so C is bit-identical whichever Gram path is taken.
+// stream without E, so C is bit-identical whichever Gram path is taken (given the same scratch:
+// the row-chunk count depends on it). scratch: nscratch bytes for the chunk partials (the Gram
+// workspace's slice area, overwritten by the slicing afterwards), or nullptr for one chunk.
 static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, int d, const double* Y, int64_t ldy,
-                     int m, int* E, int mp, double* C, cudaStream_t st) {
-  dim3 grid(((E ? mp : d) + 31) / 32, nblocks);
+                     int m, int* E, int mp, double* C, void* scratch, size_t nscratch, cudaStream_t st) {
+  RP_REQUIRE(m >= 1 && m <= 16, "gram prep: m=%d outside [1, 16]", m);
+  // row chunks: ~4 waves of 1024-column CTAs, as many as the scratch holds
+  const size_t per_chunk = sizeof(double) * (size_t)nblocks * (m + 1) * d;
+  int nchunk = 32;
+  if (rows < 256) nchunk = 1;
+  while (nchunk > 1 && (scratch == nullptr || per_chunk * nchunk > nscratch || rows / nchunk < 64)) nchunk /= 2;
+  double* Cp = reinterpret_cast<double*>(scratch);
+  double* Mp = Cp ? Cp + (size_t)nblocks * nchunk * m * d : nullptr;
+  dim3 grid((d + 1023) / 1024, nchunk, nblocks);
   switch (m) {
 #define RP_GPREP(M) \
-  case M: oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, mp, E, C); break;
+  case M:           \
+    oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, E, C); \
+    break;
     RP_GPREP(1) RP_GPREP(2) RP_GPREP(3) RP_GPREP(4) RP_GPREP(5) RP_GPREP(6) RP_GPREP(7) RP_GPREP(8)
     RP_GPREP(9) RP_GPREP(10) RP_GPREP(11) RP_GPREP(12) RP_GPREP(13) RP_GPREP(14) RP_GPREP(15) RP_GPREP(16)
 #undef RP_GPREP
-    default: return set_error(RP_EINVAL, "gram prep: m=%d outside [1, 16]", m);
   }
   RP_LAUNCH_CHECK("gram prep");
+  if (nchunk > 1) {
+    oz_gram_prep_reduce_kernel<<<dim3((mp + 255) / 256, nblocks), 256, 0, st>>>(Cp, Mp, d, m, nchunk, mp, E, C);
+    RP_LAUNCH_CHECK("gram prep reduce");
+  }
   return RP_OK;
 }
 
@@ -661,7 +676,10 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
     // one pass over X for the row exponents of the slicing and C_b = X_b^T Y_b, then the SYRK
     {
       ProfScope prof("gram_prep", st);
-      int rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, reinterpret_cast<int*>(work), oz_mp(d), C, st);
+      const size_t eb = oz_eb(oz_mp(d), nblocks);
+      const size_t ws = rp_gram_workspace_size(d, rows_per_block, nblocks);
+      int rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, reinterpret_cast<int*>(work), oz_mp(d), C,
+                         reinterpret_cast<uint8_t*>(work) + eb, ws - eb, st);
       if (rc) return rc;
     }
     return oz_syrk(oin, G, d, (int64_t)d * d, false, work, st, "oz_syrk", true);
@@ -670,7 +688,10 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
                  : gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
   if (rc) return rc;
   if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
-    rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, nullptr, d, C, xs);
+    const size_t eb = work ? oz_eb(oz_mp(d), nblocks) : 0;
+    const size_t ws = work ? rp_gram_workspace_size(d, rows_per_block, nblocks) : 0;
+    rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, nullptr, d, C,
+                   work ? reinterpret_cast<uint8_t*>(work) + eb : nullptr, ws - eb, xs);
     if (rc) return rc;
     cudaEventRecord(join, xs);
     cudaStreamWaitEvent(st, join, 0);

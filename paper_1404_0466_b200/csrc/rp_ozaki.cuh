@@ -101,59 +101,85 @@ __global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E) {
 
 // Gram blocks: the row exponents of A_b = X_b^T fused with C_b = X_b^T Y_b (both need one pass
 // over X_b; done separately they read X twice more than the slicing does). X_b row-major
-// (rows x d, leading dimension ldx), Y_b row-major (rows x m, ldy). One CTA per 32 columns of X_b:
-// 8 warps stride over the rows (lane = column: every row read is a coalesced 256-byte segment, the
-// Y row is a broadcast), then the max and the per-warp sums are combined in a fixed order.
-// E[b][i] as oz_rowexp_kernel (stride mp, rows i >= d get 0; E = nullptr: X^T Y only, the FP64
-// Gram's side stream); C[b][o][i] (column-major d x m). The same X^T Y summation order either way.
+// (rows x d, leading dimension ldx), Y_b row-major (rows x m, ldy). CTA = (1024 columns, a chunk
+// of rows, block): 256 threads x 4 columns (consecutive threads on consecutive columns, so every
+// row read is coalesced and each Y row is one broadcast for 4 columns). Per chunk the rows are
+// summed in order; with nchunk > 1 the chunk partials (sums, |max| with +inf marking NaN/inf) go
+// to Cp / Mp and oz_gram_prep_reduce_kernel combines them in chunk order, with nchunk == 1 the
+// kernel writes C and E itself. E[b][i] as oz_rowexp_kernel (stride mp, rows i >= d get 0;
+// E = nullptr: X^T Y only, the FP64 Gram's side stream); C[b][o][i] column-major d x m.
+RP_DEVINL int oz_exp_code(double mx) {  // mx = +inf marks a NaN/inf entry
+  if (!(mx <= 1.79769313486231570e308)) return OZ_NONFINITE;
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  return e;
+}
+
 template <int MT>
 __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int64_t ldx, int64_t rows, int d,
-                                                           const double* Y, int64_t ldy, int m, int mp, int* E,
-                                                           double* C) {
+                                                           const double* Y, int64_t ldy, int m, int nchunk,
+                                                           double* Cp, double* Mp, int mp, int* E, double* C) {
   constexpr int MM = MT > 0 ? MT : 1;
-  __shared__ double smx[8][32];
-  __shared__ int sfin[8][32];
-  __shared__ double ssum[8][MM][32];
-  const int b = blockIdx.y, lane = threadIdx.x & 31, wk = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + lane;
-  double mx = 0.0, acc[MM];
+  const int b = blockIdx.z, ch = blockIdx.y;
+  const int i0 = blockIdx.x * 1024 + threadIdx.x;
+  const int64_t r0 = rows * ch / nchunk, r1 = rows * (ch + 1) / nchunk;
+  double acc[4][MM], mx[4];
 #pragma unroll
-  for (int o = 0; o < MM; ++o) acc[o] = 0.0;
-  bool finite = true;
-  if (i < d) {
-    const double* x = X + (int64_t)b * rows * ldx + i;
-    const double* y = Y + (int64_t)b * rows * ldy;
-#pragma unroll 4
-    for (int64_t r = wk; r < rows; r += 8) {
-      const double xv = __ldcs(x + r * ldx);
-      const double v = fabs(xv);
-      finite &= (v <= 1.79769313486231570e308);
-      mx = fmax(mx, v);
-      const double* yr = y + r * ldy;
+  for (int j = 0; j < 4; ++j) {
+    mx[j] = 0.0;
 #pragma unroll
-      for (int o = 0; o < MM; ++o) acc[o] = fma(xv, __ldg(yr + o), acc[o]);
+    for (int o = 0; o < MM; ++o) acc[j][o] = 0.0;
+  }
+  const double* x = X + (int64_t)b * rows * ldx + i0;
+  const double* y = Y + (int64_t)b * rows * ldy;
+#pragma unroll 2
+  for (int64_t r = r0; r < r1; ++r) {
+    double yv[MM];
+#pragma unroll
+    for (int o = 0; o < MM; ++o) yv[o] = __ldg(y + r * ldy + o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + 256 * j < d) {
+        const double xv = __ldcs(x + r * ldx + 256 * j);
+        const double av = fabs(xv);
+        mx[j] = (av <= 1.79769313486231570e308) ? fmax(mx[j], av) : __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+        for (int o = 0; o < MM; ++o) acc[j][o] = fma(xv, yv[o], acc[j][o]);
+      }
     }
   }
-  smx[wk][lane] = mx;
-  sfin[wk][lane] = finite ? 1 : 0;
 #pragma unroll
-  for (int o = 0; o < MM; ++o) ssum[wk][o][lane] = acc[o];
-  __syncthreads();
-  if (E != nullptr && wk == 0 && i < mp) {
-    for (int w = 1; w < 8; ++w) {
-      mx = fmax(mx, smx[w][lane]);
-      finite = finite && sfin[w][lane];
+  for (int j = 0; j < 4; ++j) {
+    const int i = i0 + 256 * j;
+    if (nchunk == 1) {
+      if (E != nullptr && i < mp) E[(int64_t)b * mp + i] = i < d ? oz_exp_code(mx[j]) : 0;
+      if (i < d)
+        for (int o = 0; o < m; ++o) C[((int64_t)b * m + o) * d + i] = acc[j][o];
+    } else if (i < d) {
+      Mp[((int64_t)b * nchunk + ch) * d + i] = mx[j];
+      for (int o = 0; o < m; ++o) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
     }
-    int e = 0;
-    if (mx > 0.0) frexp(mx, &e);
-    E[(int64_t)b * mp + i] = (i < d && !finite) ? OZ_NONFINITE : e;
   }
-  if (i < d) {
-    for (int o = wk; o < m; o += 8) {
-      double sacc = 0.0;
-      for (int w = 0; w < 8; ++w) sacc += ssum[w][o][lane];
-      C[((int64_t)b * m + o) * d + i] = sacc;
-    }
+}
+
+__global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, int d, int m, int nchunk, int mp,
+                                           int* E, double* C) {
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= mp) return;
+  if (i >= d) {
+    if (E != nullptr) E[(int64_t)b * mp + i] = 0;
+    return;
+  }
+  if (E != nullptr) {
+    double mx = 0.0;
+    for (int c = 0; c < nchunk; ++c) mx = fmax(mx, Mp[((int64_t)b * nchunk + c) * d + i]);
+    E[(int64_t)b * mp + i] = oz_exp_code(mx);
+  }
+  for (int o = 0; o < m; ++o) {
+    double s = 0.0;
+    for (int c = 0; c < nchunk; ++c) s += Cp[(((int64_t)b * nchunk + c) * m + o) * d + i];
+    C[((int64_t)b * m + o) * d + i] = s;
   }
 }
 
