@@ -676,6 +676,7 @@ constexpr int OZ_PSLICE_B = 64 * OZ_BK;                     // bytes of one 64 x
 constexpr int OZ_PSTAGE = OZ_S * (OZ_SLICE + OZ_PSLICE_B);  // A (128 rows) and B half (64 rows), all slices
 constexpr int OZ_PSTAGES = 4;
 constexpr size_t OZ_PSMEM = 1024 + (size_t)OZ_PSTAGES * OZ_PSTAGE + 128;
+constexpr size_t OZ_PSMEM_DOT = OZ_PSMEM + 4 * 128 * 8;  // + the hold-out row reduction
 
 // Pair units of one matrix: sub-tile-row pair I2 (rows 2 I2, 2 I2 + 1), column tiles J <= 2 I2 + 1
 // (J < mt): 2 I2 + 2 units per full pair row, I2^2 + I2 before row I2.
@@ -1230,18 +1231,210 @@ __global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
+// CTA-pair hold-out kernel: as oz_dotb_kernel, but a 2-CTA cluster computes sub-tile rows 2 I2
+// and 2 I2 + 1 of T_b against the 128 columns J of W_b^T with tcgen05.mma.cta_group::2 (M = 256,
+// N = 128); each CTA stages its own 128 rows of T and 64 of the 128 W^T rows (the barrier
+// protocol of oz_syrk_pair_kernel). K runs to 128 (2 I2 + 2) for both rows of the pair (T is
+// lower triangular, so the even row's extra K block multiplies zeros). Each CTA reduces its own
+// sub-tile row into part[b][I][n].
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
+    oz_dotb_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        OzDotArgs a) {
+  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_PSTAGES * OZ_PSTAGE);
+  uint64_t* empty = full + OZ_PSTAGES;
+  uint64_t* tfull = empty + OZ_PSTAGES;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* red = reinterpret_cast<double*>(smem + OZ_PSTAGES * OZ_PSTAGE + 128);  // [4][128]
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = oz_cluster_rank();
+  const int mt2 = (a.mtA + 1) / 2;
+  const int per_I = a.nbatch * a.ntB;
+  auto decode = [&](int unit, int& b, int& I2, int& J) {  // heaviest (largest I2) first
+    const int r = unit / per_I, rem = unit - r * per_I;
+    I2 = mt2 - 1 - r;
+    b = rem / a.ntB;
+    J = rem - b * a.ntB;
+  };
+  auto ksteps = [&](int I2) {
+    const int64_t ke = (int64_t)(2 * I2 + 2) * OZ_BM < a.kpad ? (int64_t)(2 * I2 + 2) * OZ_BM : a.kpad;
+    return (int)(ke / OZ_BK);
+  };
+  const int unit0 = blockIdx.x / 2, ustep = gridDim.x / 2;
+
+  if (tid == 0) {
+    for (int s = 0; s < OZ_PSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_cluster_sync();
+  oz_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t full_leader = oz_mapa(smem_u32(full), 0);
+  const uint32_t tempty_leader = oz_mapa(smem_u32(tempty), 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
+        int b, I2, J;
+        decode(u, b, I2, J);
+        const int ba = a.a_shared ? 0 : b;
+        const int rowA = ba * OZ_S * a.MpadA + (2 * I2 + (int)rank) * OZ_BM;
+        const int rowB = b * OZ_S * a.MpadB + J * OZ_BM + (int)rank * 64;
+        const int nk = ksteps(I2);
+        for (int pass = 1; pass >= 0; --pass) {
+          const int ns = pass ? OZ_S : OZ_GP;
+          for (int kk = 0; kk < nk; ++kk, ++it) {
+            const int st = it % OZ_PSTAGES;
+            oz_mbar_wait_cluster(&empty[st], ((it / OZ_PSTAGES) & 1) ^ 1);
+            if (rank == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * (OZ_SLICE + OZ_PSLICE_B)));
+            uint8_t* sa = smem + st * OZ_PSTAGE;
+            uint8_t* sb = sa + OZ_S * OZ_SLICE;
+            const uint32_t fb = full_leader + (uint32_t)(st * 8);
+            for (int p = 0; p < ns; ++p) {
+              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, kk * OZ_BK, rowA + p * a.MpadA, fb);
+              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, kk * OZ_BK, rowB + p * a.MpadB, fb);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // the whole warp runs the loop, one elected lane issues
+      int it = 0, item = 0;
+      for (int u = unit0; u < a.total_tiles; u += ustep) {
+        int b, I2, J;
+        decode(u, b, I2, J);
+        const int nk = ksteps(I2);
+        for (int pass = 1; pass >= 0; --pass, ++item) {
+          oz_mbar_wait_cluster(tempty, (item & 1) ^ 1);
+          oz_fence_after();
+          for (int kk = 0; kk < nk; ++kk, ++it) {
+            const int st = it % OZ_PSTAGES;
+            oz_mbar_wait_cluster(&full[st], (it / OZ_PSTAGES) & 1);
+            oz_fence_after();
+            const uint32_t sa = smem_u32(smem + st * OZ_PSTAGE);
+            const uint32_t sb = sa + OZ_S * OZ_SLICE;
+            if (pass)
+              oz_issue_kstep<OZ_GP, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
+            else
+              oz_issue_kstep<0, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
+            oz_commit_pair(&empty[st]);
+          }
+          oz_commit_pair(tfull);
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3, chalf = (warp - 2) >> 2;
+    const int row_in_tile = quarter * 32 + lane;
+    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
+    int item = 0;
+    for (int u = unit0; u < a.total_tiles; u += ustep) {
+      int b, I2, J;
+      decode(u, b, I2, J);
+      const int I = 2 * I2 + (int)rank;
+      const bool valid = I < a.mtA;
+      const int ba = a.a_shared ? 0 : b;
+      const int i = I * OZ_BM + row_in_tile;
+      const int ei = a.EA[(int64_t)ba * a.MpadA + i];
+      const int* EBb = a.EB + (int64_t)b * a.MpadB;
+      const double* Wrow = a.W + (int64_t)b * a.w_stride + (int64_t)i * a.ldw;
+      double acc[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+      for (int pass = 1; pass >= 0; --pass, ++item) {
+        const int g0 = pass * OZ_GP;
+        oz_mbar_wait_cluster(tfull, item & 1);
+        oz_fence_after();
+#pragma unroll
+        for (int g = OZ_GP - 1; g >= 0; --g) {
+          if (g0 + g >= OZ_S) continue;
+          const double w = ldexp(1.0, -8 * (g0 + g) - 12);
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t t[16];
+            oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), t);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)t[c], w, acc[q4 * 16 + c]);
+          }
+        }
+        oz_fence_before();
+        __syncwarp();
+        if (lane == 0) oz_mbar_arrive_remote(tempty_leader);
+      }
+      const int n0 = J * OZ_BM + chalf * 64;
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const int n = n0 + c;
+        double x = 0.0;
+        if (valid && i < a.d && n < a.N) {
+          const int en = EBb[n];
+          x = (ei == OZ_NONFINITE || en == OZ_NONFINITE) ? __longlong_as_double(0x7ff8000000000000LL)
+                                                          : ldexp(acc[c], ei + en) * Wrow[n];
+        }
+        acc[c] = x;
+      }
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
+          const bool upper = (lane & s2) != 0;
+#pragma unroll
+          for (int j = 0; j < s2; ++j) {
+            const double send = upper ? acc[hh * 32 + j] : acc[hh * 32 + j + s2];
+            const double keep = upper ? acc[hh * 32 + j + s2] : acc[hh * 32 + j];
+            acc[hh * 32 + j] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
+          }
+        }
+        red[quarter * 128 + chalf * 64 + hh * 32 + lane] = acc[hh * 32];
+      }
+      named_bar_sync(1, 256);
+      if (quarter == 0 && valid) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int col = chalf * 64 + hh * 32 + lane;
+          const double tot = red[col] + red[128 + col] + red[256 + col] + red[384 + col];
+          const int n = J * OZ_BM + col;
+          if (n < a.N) a.part[((int64_t)b * a.mtA + I) * a.N + n] = tot;
+        }
+      }
+      named_bar_sync(1, 256);
+    }
+  }
+  oz_fence_before();
+  __syncthreads();
+  oz_cluster_sync();
+  oz_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 inline int64_t oz_rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 // Workspace of oz_holdout: exponents and slices of T (nA copies) and of W^T (nbatch).
 inline size_t oz_holdout_workspace(int d, int64_t N, int nbatch, bool a_shared) {
-  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
+  const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = a_shared ? 1 : nbatch;
   return (size_t)oz_rup((int64_t)na * mpa * 4, 1024) + (size_t)oz_rup((int64_t)nbatch * mpb * 4, 1024) +
          (size_t)na * OZ_S * mpa * kpad + (size_t)nbatch * OZ_S * mpb * kpad;
 }
 
 inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
-  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM);
+  const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM);
   return oz_kpad(d) <= oz_kchunk(oz_kpad(d)) && (int64_t)nbatch * OZ_S * (mpa > mpb ? mpa : mpb) < 0x7fffffff &&
          oz_encode_fn() != nullptr;
 }
@@ -1250,7 +1443,8 @@ inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
 inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
                       int64_t N, int nbatch, double* part, void* work, cudaStream_t st) {
   const bool shared = g_stride == 0;
-  const int64_t mpa = oz_rup(d, OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
+  const bool pair = oz_pair_enabled();
+  const int64_t mpa = oz_rup(d, pair ? 256 : OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = shared ? 1 : nbatch;
   uint8_t* w8 = reinterpret_cast<uint8_t*>(work);
   int* EA = reinterpret_cast<int*>(w8);
@@ -1269,7 +1463,8 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   rc = oz_prepare(ib, EB, SB, kpad, st);
   if (rc) return rc;
   CUtensorMap ta, tb;
-  if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) || !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb))
+  if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) ||
+      !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb, pair ? 64 : OZ_BM))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
   OzDotArgs a;
   a.EA = EA;
@@ -1282,18 +1477,24 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   a.N = (int)N;
   a.MpadA = (int)mpa;
   a.MpadB = (int)mpb;
-  a.mtA = (int)(mpa / OZ_BM);
+  a.mtA = (int)(oz_rup(d, OZ_BM) / OZ_BM);
   a.ntB = (int)(mpb / OZ_BM);
   a.nbatch = nbatch;
   a.a_shared = shared ? 1 : 0;
-  a.total_tiles = a.mtA * a.ntB * nbatch;
+  a.total_tiles = (pair ? (a.mtA + 1) / 2 : a.mtA) * a.ntB * nbatch;
   a.kpad = kpad;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = a.total_tiles < sms ? a.total_tiles : sms;
-  cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
-  {
+  if (pair) {
+    int pairs = sms / 2;
+    if (pairs > a.total_tiles) pairs = a.total_tiles;
+    cudaFuncSetAttribute(oz_dotb_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM_DOT);
+    ProfScope prof("oz_holdout", st);
+    oz_dotb_pair_kernel<<<2 * pairs, OZ_SYRK_THREADS, OZ_PSMEM_DOT, st>>>(ta, tb, a);
+  } else {
+    const int grid = a.total_tiles < sms ? a.total_tiles : sms;
+    cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
     ProfScope prof("oz_holdout", st);
     oz_dotb_kernel<<<grid, OZ_SYRK_THREADS, OZ_SMEM, st>>>(ta, tb, a);
   }
