@@ -39,7 +39,9 @@ def _newest(paths):
 
 
 def _compile(src, obj, verbose):
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+    # RP_NVCC_EXTRA: extra flags for experiments (e.g. -DRP_SOLVE_PROF); not used by the product build
+    extra = os.environ.get("RP_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

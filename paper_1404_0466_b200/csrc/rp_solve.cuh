@@ -21,9 +21,28 @@
 //    column, reading its coefficients through the read-only path (uniform addresses ->
 //    broadcast). The diagonal pass also raises the SingularInterpolant flag.
 #pragma once
+#include <cstdio>
+
 #include "rp_common.cuh"
 
 namespace rp {
+
+// RP_SOLVE_PROF (experiments only): per-phase clock64 totals of the diagonal steps of CTA 0,
+// printed when the kernel ends.
+#ifdef RP_SOLVE_PROF
+#define RP_SP_MARK(k)                              \
+  do {                                             \
+    if (tid == 0) {                                \
+      const long long _t = clock64();              \
+      sp_acc[k] += _t - sp_last;                   \
+      sp_last = _t;                                \
+    }                                              \
+  } while (0)
+#else
+#define RP_SP_MARK(k) \
+  do {                \
+  } while (0)
+#endif
 
 constexpr int SOLVE_LC = 16;          // max lambdas per CTA (specialised kernels)
 constexpr int SOLVE_LC_GENERIC = 8;   // max lambdas per CTA (generic kernel)
@@ -102,6 +121,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   __syncthreads();
   int it0 = 0;  // slabs consumed by earlier rows (stage / phase bookkeeping)
 
+#ifdef RP_SOLVE_PROF
+  long long sp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sp_last = clock64();
+#endif
   double tl[LH];
 #pragma unroll
   for (int i = 0; i < LH; ++i) {
@@ -115,6 +137,11 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   for (int step = 0; step < a.nt; ++step) {
     const int I = BWD ? (a.nt - 1 - step) : step;
     const int nslab = (a.dbg & 4) ? 0 : 4 * (BWD ? (a.nt - 1 - I) : I);  // dbg 4: diagonal steps only
+    if (tid == 0) {  // warm L2 with this row's diagonal tile: its copy at the end of the row then hits
+      const double* dt = theta + (int64_t)tile_index(I, I) * P * TILE_PLANE;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(dt), "r"((uint32_t)(P * TILE_PLANE * 8))
+                   : "memory");
+    }
 #pragma unroll
     for (int i = 0; i < LH; ++i)
 #pragma unroll
@@ -205,6 +232,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     it0 += nslab;
     __syncthreads();  // every warp is done with the ring
+    RP_SP_MARK(0);    // slabs of the row
 
     // ---- diagonal tile: stage theta_II (P x 64 x 64, forward copy) into the drained ring,
     //      R = base - acc into sR, then a triangular solve per (lambda, output) column ----
@@ -253,6 +281,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     mbar_wait(&full[STG], step & 1);
     __syncthreads();
+    RP_SP_MARK(1);  // R = base - acc, theta_II staged
     // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows. Per 16 x 16 diagonal
     // block: evaluate it once per lambda into shared memory (with reciprocal pivots and the
     // singular check), then one thread per (lambda, output) column substitutes with its 16 rows in
@@ -267,7 +296,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       for (int e = tid; e < nl * 136; e += NTH) {
         const int l = e / 136;
         int ij = e - l * 136;  // packed lower index: row i, col j <= i
-        int i = (int)((sqrt(8.0 * ij + 1.0) - 1.0) * 0.5);
+        int i = (int)((sqrtf(8.0f * ij + 1.0f) - 1.0f) * 0.5f);  // FP32 estimate, corrected below
         while ((i + 1) * (i + 2) / 2 <= ij) ++i;
         while (i * (i + 1) / 2 > ij) --i;
         const int j = ij - i * (i + 1) / 2;
@@ -284,6 +313,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
       __syncthreads();
+      RP_SP_MARK(2);  // evaluate the 16 x 16 block
       if (!(a.dbg & 2) && tid < cw) {
         const int l = tid / m;
         const double* Lv = sLev + l * 16 * 17;
@@ -310,6 +340,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         for (int i = 0; i < 16; ++i) sR[(r0 + i) * S + tid] = x[i];
       }
       __syncthreads();
+      RP_SP_MARK(3);  // 16-row substitution
       // rows still to solve: after the block (fwd) / before it (bwd)
       if (q < 3 && (BWD ? (rg < sb) : (rg > sb))) {
 #pragma unroll
@@ -383,6 +414,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         }
       }
       __syncthreads();
+      RP_SP_MARK(4);  // DMMA update of the rows below
     }
     // publish row I: private rows (read back by later slabs through the async proxy) and, for
     // the backward pass, the caller's row-major W (overlapping chunks write identical values)
@@ -396,7 +428,14 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     __syncthreads();
+    RP_SP_MARK(5);  // publish
   }
+#ifdef RP_SOLVE_PROF
+  if (tid == 0 && blockIdx.x == 0)
+    printf("solve %s phases (Mcycles): slabs %.3f R+stage %.3f eval %.3f subst %.3f update %.3f publish %.3f\n",
+           BWD ? "bwd" : "fwd", sp_acc[0] * 1e-6, sp_acc[1] * 1e-6, sp_acc[2] * 1e-6, sp_acc[3] * 1e-6,
+           sp_acc[4] * 1e-6, sp_acc[5] * 1e-6);
+#endif
 }
 
 // Row stride of the W / R tiles: >= lam*m and = 12 (mod 16) doubles, so the DMMA B fragments
