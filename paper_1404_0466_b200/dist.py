@@ -4,7 +4,7 @@ One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). Folds are
 independent until the final mean, so fold f runs on rank f % world. Two
 exchanges are real data dependencies of the path:
 
-* Gram blocks: the training Hessian of fold f is sum_b G_b - G_f, so every
+* Gram blocks: the training Hessian of fold f is sum_{b != f} G_b, so every
   rank needs all k fold-block Grams. When k % world == 0 each rank computes only
   its own k / world blocks and the blocks are all-gathered (deterministic: every
   rank then sums them in the same fixed order, so H_f is bit-identical at any

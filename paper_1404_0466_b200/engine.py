@@ -5,7 +5,7 @@ across calls -- no allocation on the hot path) and launches the six stages of
 SURVEY.md 8(a) through the C ABI on the current torch CUDA stream:
 
   (1) rp_gram_blocks      G_b = X_b^T X_b, C_b = X_b^T Y_b per fold block   ridge.py:50-60
-      rp_fold_systems     A_{f,s} = sum_b G_b - G_f + lam_s I, rhs_f        pichol.py:105
+      rp_fold_systems     A_{f,s} = sum_{b != f} G_b + lam_s I, rhs_f       pichol.py:105
   (2) rp_potrf_batched    L_{f,s} = chol(A_{f,s}) for all local folds x s   linalg.py:98
   (3+4) rp_fit_tiles      theta_f = P T_f in the tile layout + residual     pichol.py:109-125
   (5) rp_eval_solve       W_f(lam_j) for all q lambdas, fused eval+solve    ridge.py:78-91
@@ -14,7 +14,7 @@ SURVEY.md 8(a) through the C ABI on the current torch CUDA stream:
 
 Folds are contiguous row blocks of the (fold-grouped) design: block b holds the
 validation rows of fold b, so the training Hessian of fold f is
-sum_b G_b - G_f. Multi-GPU sharding plugs in through the
+sum_{b != f} G_b. Multi-GPU sharding plugs in through the
 ``exchange_grams`` / ``gather_curves`` hooks (see ``dist.py``).
 """
 

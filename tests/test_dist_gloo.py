@@ -27,9 +27,9 @@ def _port():
 
 
 def _fold_curves(X, Y, Gblocks, Cblocks, f, grid):
-    """Per-fold curve from Gram blocks (sum_b G_b - G_f), like the device pipeline."""
-    H = sum(Gblocks[b] for b in range(K)) - Gblocks[f]
-    G = sum(Cblocks[b] for b in range(K)) - Cblocks[f]
+    """Per-fold curve from Gram blocks (sum_{b != f} G_b in block order), like the device pipeline."""
+    H = sum(Gblocks[b] for b in range(K) if b != f)
+    G = sum(Cblocks[b] for b in range(K) if b != f)
     model = orc.fit(H, grid[orc.sample_indices(Q, S)], R)
     rows = slice(f * (N // K), (f + 1) * (N // K))
     return np.stack([orc.holdout_error(orc.solve_interp(model, G, lam), X[rows], Y[rows]) for lam in grid])
