@@ -10,7 +10,7 @@ import json
 import subprocess
 import sys
 
-KEYS = {"oz_syrk_kernel": "oz_syrk", "oz_syrk_pair_kernel": "oz_syrk", "eval_solve_kernel": "eval_solve", "32, 3>": "holdout_gemm", "oz_dotb_kernel": "oz_holdout"}
+KEYS = {"oz_syrk_kernel": "oz_syrk", "oz_syrk_pair_kernel": "oz_syrk", "eval_solve_kernel": "eval_solve", "32, 3>": "holdout_gemm", "oz_dotb_kernel": "oz_holdout", "oz_dotb_pair_kernel": "oz_holdout"}
 
 
 def main(rep):
