@@ -66,6 +66,15 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
       pl.fast = false;
     }
   }
+  static const int lam_env = [] {  // RP_SOLVE_LAM (experiments): force a specialised chunk size
+    const char* e = getenv("RP_SOLVE_LAM");
+    return e ? atoi(e) : 0;
+  }();
+  if (lam_env > 0 && q >= lam_env && has_solve_fast(m, pl.P, lam_env) &&
+      solve_smem_bytes(lam_env, m, pl.P) <= (size_t)maxsmem) {
+    pl.lam = lam_env;
+    pl.fast = true;
+  }
   if (pl.lam > 0) {
     pl.chunks = (q + pl.lam - 1) / pl.lam;
     pl.S = solve_stride(pl.lam, m);
