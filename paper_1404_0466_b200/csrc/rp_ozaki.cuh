@@ -183,72 +183,98 @@ __global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, i
   }
 }
 
-// Digits of 64 (i) x 256 (k) of A, in four 64 x 64 sub-tiles, written K-major:
-// slices[((b*S + p)*Mpad + i)*kpad + k]. Columns past K and rows past M give zero digits.
+// Digits of 128 (i) x 256 (k) of A, in four 128 x 64 sub-tiles, written K-major:
+// slices[((b*S + p)*Mpad + i)*kpad + k]. Columns past K and rows past M give zero digits. Each
+// k of a sub-tile is one 1 KB contiguous read of A (consecutive threads on consecutive rows i);
+// a thread loads its 16 values of a half sub-tile before converting any (the kernel is bound by
+// load latency otherwise).
+constexpr int OZ_SLICE_IW = 128;
+constexpr size_t OZ_SLICE_SMEM = sizeof(uint32_t) * OZ_S * OZ_SLICE_IW * 17;
 __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, int8_t* slices, int64_t kpad) {
-  __shared__ uint32_t dig[OZ_S][64][17];  // [p][i][k/4], 4 digits per word, padded rows
-  const int b = blockIdx.z, i0 = blockIdx.y * 64;
+  constexpr int IW = OZ_SLICE_IW;
+  extern __shared__ uint32_t oz_dig_raw[];  // dig[p][i][k/4], 4 digits per word, padded rows
+  uint32_t(*dig)[IW][17] = reinterpret_cast<uint32_t(*)[IW][17]>(oz_dig_raw);
+  const int b = blockIdx.z, i0 = blockIdx.y * IW;
   const double* Ab = in.A + (int64_t)b * in.bstride;
   const int mp = in.mpad();
+  const int ii = threadIdx.x & (IW - 1), kqb = threadIdx.x / IW;  // kq = kqb + 2 * u
+  const int i = i0 + ii;
+  const int ei = (i < in.M) ? E[(int64_t)b * mp + i] : OZ_NONFINITE;
+  const double scale = ldexp(1.0, 54 - (ei == OZ_NONFINITE ? 0 : ei));  // |x| < 2^ei -> |v| < 2^54
   for (int sub = 0; sub < 4; ++sub) {
     const int64_t k0 = (int64_t)blockIdx.x * 256 + sub * 64;
     if (k0 >= kpad) break;
-    for (int it = threadIdx.x; it < 64 * 16; it += 256) {
-      const int ii = it & 63, kq = it >> 6;  // consecutive threads: consecutive rows (contiguous)
-      const int i = i0 + ii;
-      uint32_t w[OZ_S];
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      double xs[4][4];
 #pragma unroll
-      for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
-      const int ei = (i < in.M) ? E[(int64_t)b * mp + i] : OZ_NONFINITE;
-      if (ei != OZ_NONFINITE) {
-        const double scale = ldexp(1.0, 54 - ei);  // |x| < 2^ei -> |v| < 2^54
-        double xs[4];
+      for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
+          const int kq = kqb + 2 * (4 * half + u);
           const int64_t k = k0 + kq * 4 + r;
-          xs[r] = (k < in.K && (!in.tri || k <= i)) ? __ldcs(Ab + k * in.lda + i) : 0.0;
+          xs[u][r] =
+              (ei != OZ_NONFINITE && k < in.K && (!in.tri || k <= i)) ? __ldcs(Ab + k * in.lda + i) : 0.0;
         }
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int64_t k = k0 + kq * 4 + r;
-          double x = xs[r];
-          if (in.tri && k == i) x *= 0.5;  // exact
-          const long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
-          // balanced base-256 digits: with u = v + 0x808080808080, the low six bytes of u are the
-          // digits d_1..d_6 (d in [-128, 127]) offset by 128, and u >> 48 is the top digit d_0
-          // (|d_0| <= 65). Offsets are removed below by flipping each byte's top bit.
-          const unsigned long long u = (unsigned long long)(v + 0x808080808080LL);
-          const uint32_t lo = (uint32_t)u, hi = (uint32_t)(u >> 32);
-          const uint32_t sh = 8 * r;
-          w[6] |= (lo & 0xffu) << sh;
-          w[5] |= ((lo >> 8) & 0xffu) << sh;
-          w[4] |= ((lo >> 16) & 0xffu) << sh;
-          w[3] |= (lo >> 24) << sh;
-          w[2] |= (hi & 0xffu) << sh;
-          w[1] |= ((hi >> 8) & 0xffu) << sh;
-          w[0] |= ((uint32_t)((int)hi >> 16) & 0xffu) << sh;
+      for (int u = 0; u < 4; ++u) {
+        const int kq = kqb + 2 * (4 * half + u);
+        uint32_t w[OZ_S];
+#pragma unroll
+        for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
+        if (ei != OZ_NONFINITE) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int64_t k = k0 + kq * 4 + r;
+            double x = xs[u][r];
+            if (in.tri && k == i) x *= 0.5;  // exact
+            const long long v = (long long)(x * scale);  // truncation toward zero, |v| < 2^54
+            // balanced base-256 digits: with uu = v + 0x808080808080, the low six bytes of uu are
+            // the digits d_1..d_6 (d in [-128, 127]) offset by 128, and uu >> 48 is the top digit
+            // d_0 (|d_0| <= 65). Offsets are removed below by flipping each byte's top bit.
+            const unsigned long long uu = (unsigned long long)(v + 0x808080808080LL);
+            const uint32_t lo = (uint32_t)uu, hi = (uint32_t)(uu >> 32);
+            const uint32_t sh = 8 * r;
+            w[6] |= (lo & 0xffu) << sh;
+            w[5] |= ((lo >> 8) & 0xffu) << sh;
+            w[4] |= ((lo >> 16) & 0xffu) << sh;
+            w[3] |= (lo >> 24) << sh;
+            w[2] |= (hi & 0xffu) << sh;
+            w[1] |= ((hi >> 8) & 0xffu) << sh;
+            w[0] |= ((uint32_t)((int)hi >> 16) & 0xffu) << sh;
+          }
+#pragma unroll
+          for (int p = 1; p < OZ_S; ++p) w[p] ^= 0x80808080u;
         }
 #pragma unroll
-        for (int p = 1; p < OZ_S; ++p) w[p] ^= 0x80808080u;
+        for (int p = 0; p < OZ_S; ++p) dig[p][ii][kq] = w[p];
       }
-#pragma unroll
-      for (int p = 0; p < OZ_S; ++p) dig[p][ii][kq] = w[p];
     }
     __syncthreads();
-    for (int it = threadIdx.x; it < OZ_S * 64 * 4; it += 256) {
-      const int c = it & 3, ii = (it >> 2) & 63, p = it >> 8;
-      const int i = i0 + ii;
+    for (int it = threadIdx.x; it < OZ_S * IW * 4; it += 256) {
+      const int c = it & 3, ri = (it >> 2) & (IW - 1), p = it / (4 * IW);
+      const int row = i0 + ri;
       const int64_t k = k0 + c * 16;
-      if (i >= mp || k >= kpad) continue;
+      if (row >= mp || k >= kpad) continue;
       uint4 v;
-      v.x = dig[p][ii][c * 4 + 0];
-      v.y = dig[p][ii][c * 4 + 1];
-      v.z = dig[p][ii][c * 4 + 2];
-      v.w = dig[p][ii][c * 4 + 3];
-      *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * mp + i) * kpad + k) = v;
+      v.x = dig[p][ri][c * 4 + 0];
+      v.y = dig[p][ri][c * 4 + 1];
+      v.z = dig[p][ri][c * 4 + 2];
+      v.w = dig[p][ri][c * 4 + 3];
+      *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * mp + row) * kpad + k) = v;
     }
     __syncthreads();
   }
+}
+
+inline cudaError_t oz_slice_launch(const OzIn& in, const int* E, int8_t* slices, int64_t kpad, cudaStream_t st) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(oz_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SLICE_SMEM);
+  if (attr != cudaSuccess) return attr;
+  const int mp = in.mpad();
+  oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + OZ_SLICE_IW - 1) / OZ_SLICE_IW, in.nbatch), 256,
+                    OZ_SLICE_SMEM, st>>>(in, E, slices, kpad);
+  return cudaSuccess;  // launch errors are picked up by the caller's RP_LAUNCH_CHECK
 }
 
 // ------------------------------------------------------------------ tcgen05 helpers
@@ -911,15 +937,12 @@ inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cuda
   const int mp = in.mpad();
   oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E);
   RP_LAUNCH_CHECK("ozaki rowexp");
-  oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(in, E, slices,
-                                                                                                  kpad);
+  cudaError_t e = oz_slice_launch(in, E, slices, kpad, st);
+  if (e != cudaSuccess) return cuda_status(e, "ozaki slice attributes");
   RP_LAUNCH_CHECK("ozaki slice");
   return RP_OK;
 }
 
-// C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
-// exps_ready: the row exponents are already in the workspace (E[b * oz_mp(M) + i], e.g. from
-// oz_gram_prep_kernel), so only the slicing pass runs.
 // RP_OZAKI_PAIR=0: independent CTAs (128 x 128 tiles) instead of CTA pairs (256 x 128 blocks)
 inline bool oz_pair_enabled() {
   static const bool pair = [] {
@@ -929,6 +952,9 @@ inline bool oz_pair_enabled() {
   return pair;
 }
 
+// C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
+// exps_ready: the row exponents are already in the workspace (E[b * oz_mp(M) + i], e.g. from
+// oz_gram_prep_kernel), so only the slicing pass runs.
 inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
                    cudaStream_t st, const char* prof_name = "oz_syrk", bool exps_ready = false) {
   const bool pair = oz_pair_enabled();
@@ -941,8 +967,8 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   {
     ProfScope prof("oz_prep", st);
     if (exps_ready && pair) {
-      oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + 63) / 64, in.nbatch), 256, 0, st>>>(pin, E, slices,
-                                                                                                      kpad);
+      cudaError_t e = oz_slice_launch(pin, E, slices, kpad, st);
+      if (e != cudaSuccess) return cuda_status(e, "ozaki slice attributes");
       RP_LAUNCH_CHECK("ozaki slice");
     } else {
       int rc = oz_prepare(pin, E, slices, kpad, st);
