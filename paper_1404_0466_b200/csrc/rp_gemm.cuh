@@ -376,6 +376,18 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
       const double* A = p.A + tc.batch * p.strideA;
       const double* B = p.B + tc.batch * p.strideB;
       const int ktiles = ktiles_of(tc.tm);
+      if (EPI == EPI_STORE && p.beta != 0.0) {
+        // warm L2 with the C tile the epilogue will read: its loads then hit L2 instead of HBM
+        // (with short K the epilogue is a large share of a tile, and the consumers wait on it)
+        const double* Ct = p.C + tc.batch * p.strideC + (int64_t)n0 * p.ldc + m0;
+        const uint32_t bytes = (uint32_t)(mv * 8);
+        if ((bytes & 15) == 0)
+          for (int c = lane; c < nv; c += 32) {
+            const double* col = Ct + (int64_t)c * p.ldc;
+            if (((uintptr_t)col & 15) == 0)
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(col), "r"(bytes) : "memory");
+          }
+      }
       for (int kt = 0; kt < ktiles; ++kt, ++it) {
         const int st = it % WS_STAGES;
         mbar_wait(&empty[st], ((it / WS_STAGES) & 1) ^ 1);
