@@ -284,13 +284,17 @@ class PicholEngine:
         self.stage_holdout(X, Y)
         mark("predict_local")
         curves_all = gather_curves(self.curves) if gather_curves is not None else self.curves
-        self.stage_select(curves_all)
+        # the fold mean needs every fold's curve: a device holding only some folds and no gather
+        # hook returns its local curves without a selection
+        complete = curves_all.shape[0] == self.k
+        if complete:
+            self.stage_select(curves_all)
         mark("predict")
         if ev is not None:
             torch.cuda.synchronize()
             for (n0, e0), (n1, e1) in zip(ev[:-1], ev[1:]):
                 timings[n1] = timings.get(n1, 0.0) + e0.elapsed_time(e1) / 1e3
-        return curves_all, self.mean, self.best
+        return (curves_all, self.mean, self.best) if complete else (curves_all, None, None)
 
     def check_numerics(self, sample_lams):
         """Raise the reference's exceptions for device-side failures (host sync)."""

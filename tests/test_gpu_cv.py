@@ -169,3 +169,35 @@ def test_session_streamed_upload_matches_resident_sweep(gpu, k):
     assert np.array_equal(best_s, best_r)
     ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(600 * k, k), k, grid.values, g=4, r=2)
     assert rel(curves_s, ref["curves"]) <= 1e-8
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_rank_view_is_bit_identical_to_the_full_sweep(gpu, world):
+    """Each rank of a fold-sharded run (dist.Shard) computes only its folds, and only its own
+    Gram blocks (the others arrive by all-gather). Emulated on one GPU: the per-rank engine gets
+    the other blocks copied in, as the all-gather would; its curves must equal the full sweep's
+    curves of the same folds bit for bit (fixed per-fold arithmetic, fixed-order sums)."""
+    from paper_1404_0466_b200 import dist
+
+    cfg = configs.CONFIGS["c4"].scaled(n=2400, d=256, m=3, q=9)
+    X, Y = configs.generate(cfg)
+    grid = configs.grid_values(cfg)
+    lams, V, _, ts, tsh, P = pichol.fit_basis(grid[orc.sample_indices(cfg.q, cfg.s)], cfg.r)
+    dX, dY = _dev.to_dev(X), _dev.to_dev(Y)
+    full = PicholEngine([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, cfg.q, cfg.s, cfg.r)
+    curves_full, _, _ = full.sweep(dX, dY, lams, P, V, ts * grid + tsh)
+    curves_full = curves_full.cpu().numpy()
+    for rank in range(world):
+        sh = dist.Shard(rank, world, cfg.k)
+        eng = PicholEngine([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, cfg.q, cfg.s, cfg.r,
+                           local_folds=sh.local_folds, gram_blocks=sh.gram_blocks)
+
+        def exchange(e, src=full, blocks=sh.gram_blocks):
+            for b in range(cfg.k):
+                if b not in blocks:  # what all_gather_into_tensor delivers from the other ranks
+                    e.G[b].copy_(src.G[b])
+                    e.C[b].copy_(src.C[b])
+                    e.yy[b].copy_(src.yy[b])
+
+        curves, _, _ = eng.sweep(dX, dY, lams, P, V, ts * grid + tsh, exchange_grams=exchange)
+        assert np.array_equal(curves.cpu().numpy(), curves_full[sh.local_folds]), (world, rank)
