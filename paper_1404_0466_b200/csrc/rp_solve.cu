@@ -52,7 +52,10 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
     const int chunks = (q + lam - 1) / lam;
     const long long ctas = (long long)nf * chunks;
     const double waves = (double)((ctas + sms - 1) / sms);
-    const double base = waves * lam * (1.0 + 0.02 * (SOLVE_LC - lam));
+    // per-lambda cost grows as chunks shrink (every CTA streams all of its fold's theta and runs
+    // all diagonal steps): measured per-lambda time at c5 (m = 16, degree 3) 16.5 / 13.7 / 13.0
+    // for 4 / 6 / 8 lambdas per CTA, i.e. ~1 + 0.1 (16 - lam) relative to a full chunk
+    const double base = waves * lam * (1.0 + 0.1 * (SOLVE_LC - lam));
     const bool fast_ok = q >= lam && has_solve_fast(m, pl.P, lam) && ((m % 2 == 0) || ((q - lam) % 2 == 0));
     const bool gen_ok = lam <= SOLVE_LC_GENERIC && !((m & 1) && (lam & 1) && q > 1);  // odd m: even chunks
     if (fast_ok && base < best_cost - 1e-9) {
