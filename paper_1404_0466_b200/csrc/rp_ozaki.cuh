@@ -151,13 +151,19 @@ __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int6
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int i = i0 + 256 * j;
+    // compile-time bound on o (a runtime bound would index acc dynamically: local memory)
     if (nchunk == 1) {
       if (E != nullptr && i < mp) E[(int64_t)b * mp + i] = i < d ? oz_exp_code(mx[j]) : 0;
-      if (i < d)
-        for (int o = 0; o < m; ++o) C[((int64_t)b * m + o) * d + i] = acc[j][o];
+      if (i < d) {
+#pragma unroll
+        for (int o = 0; o < MM; ++o)
+          if (o < m) C[((int64_t)b * m + o) * d + i] = acc[j][o];
+      }
     } else if (i < d) {
       Mp[((int64_t)b * nchunk + ch) * d + i] = mx[j];
-      for (int o = 0; o < m; ++o) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
+#pragma unroll
+      for (int o = 0; o < MM; ++o)
+        if (o < m) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
     }
   }
 }
