@@ -558,10 +558,19 @@ static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, in
   double* Cp = reinterpret_cast<double*>(scratch);
   double* Mp = Cp ? Cp + (size_t)nblocks * nchunk * m * d : nullptr;
   dim3 grid((d + 1023) / 1024, nchunk, nblocks);
+  // X rows streamed by bulk copies when every row segment is 16-byte aligned
+  const bool bulk = ((uintptr_t)X & 15) == 0 && ldx % 2 == 0 && d % 2 == 0;
   switch (m) {
-#define RP_GPREP(M) \
-  case M:           \
-    oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, E, C); \
+#define RP_GPREP(M)                                                                                            \
+  case M:                                                                                                      \
+    if (bulk) {                                                                                                \
+      cudaFuncSetAttribute(oz_gram_prep_bulk_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                           (int)OZ_GP_SMEM);                                                                   \
+      oz_gram_prep_bulk_kernel<M><<<grid, 256, OZ_GP_SMEM, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, \
+                                                                 E, C);                                        \
+    } else {                                                                                                   \
+      oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, E, C);     \
+    }                                                                                                          \
     break;
     RP_GPREP(1) RP_GPREP(2) RP_GPREP(3) RP_GPREP(4) RP_GPREP(5) RP_GPREP(6) RP_GPREP(7) RP_GPREP(8)
     RP_GPREP(9) RP_GPREP(10) RP_GPREP(11) RP_GPREP(12) RP_GPREP(13) RP_GPREP(14) RP_GPREP(15) RP_GPREP(16)
