@@ -87,6 +87,10 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   constexpr int NTA = NT > 0 ? NT : 1;
   constexpr bool REM2 = (REM % 2) == 0;
   extern __shared__ __align__(16) double smem[];
+  // diagonal-block helpers (static): packed lower index -> (row, col) of a 16 x 16 block, and the
+  // chunk's t values
+  __shared__ uint8_t s_pi[136], s_pj[136];
+  __shared__ double s_tv[LCT ? LCT : SOLVE_LC_GENERIC];
   const int P = PT ? PT : a.P;
   const int S = a.S, m = a.m;
   const int stageT = P * FWD_SLAB;  // both directions: [k][68] slabs (bwd from the transposed copy)
@@ -124,6 +128,13 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 #ifdef RP_SOLVE_PROF
   long long sp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sp_last = clock64();
 #endif
+  for (int e = tid; e < 136; e += NTH) {
+    int i = 0;
+    while ((i + 1) * (i + 2) / 2 <= e) ++i;
+    s_pi[e] = (uint8_t)i;
+    s_pj[e] = (uint8_t)(e - i * (i + 1) / 2);
+  }
+  for (int l = tid; l < nl; l += NTH) s_tv[l] = a.tvals[l0 + l];
   double tl[LH];
 #pragma unroll
   for (int i = 0; i < LH; ++i) {
@@ -295,12 +306,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       const int r0 = sb * 16;
       for (int e = tid; e < nl * 136; e += NTH) {
         const int l = e / 136;
-        int ij = e - l * 136;  // packed lower index: row i, col j <= i
-        int i = (int)((sqrtf(8.0f * ij + 1.0f) - 1.0f) * 0.5f);  // FP32 estimate, corrected below
-        while ((i + 1) * (i + 2) / 2 <= ij) ++i;
-        while (i * (i + 1) / 2 > ij) --i;
-        const int j = ij - i * (i + 1) / 2;
-        const double tv = a.tvals[l0 + l];
+        const int ij = e - l * 136;  // packed lower index: row i, col j <= i
+        const int i = s_pi[ij], j = s_pj[ij];
+        const double tv = s_tv[l];
         const int off = (r0 + j) * TILE_LD + r0 + i;  // L(r0+i, r0+j), forward (column-major) copy
         double v = 0.0;
 #pragma unroll
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           if (p < P) v = (p == P - 1) ? sD[p * TILE_PLANE + off] : fma(v, tv, sD[p * TILE_PLANE + off]);
         sLev[(l * 16 + i) * 17 + j] = v;
         if (i == j) {
-          sRinv[l * 16 + i] = 1.0 / v;
+          sRinv[l * 16 + i] = __drcp_rn(v);  // = 1.0 / v (correctly rounded), without the division path
           if (!BWD && rowI + r0 + i < a.d && !(fabs(v) >= 1e-12)) a.flags[fold * a.q + l0 + l] = 1;
         }
       }
