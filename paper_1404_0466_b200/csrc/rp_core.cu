@@ -559,7 +559,8 @@ static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, in
   double* Mp = Cp ? Cp + (size_t)nblocks * nchunk * m * d : nullptr;
   dim3 grid((d + 1023) / 1024, nchunk, nblocks);
   // X rows streamed by bulk copies when every row segment is 16-byte aligned
-  const bool bulk = ((uintptr_t)X & 15) == 0 && ldx % 2 == 0 && d % 2 == 0;
+  const bool bulk = ((uintptr_t)X & 15) == 0 && ldx % 2 == 0 && d % 2 == 0 && ((uintptr_t)Y & 15) == 0 &&
+                    ldy % 2 == 0 && m % 2 == 0;
   switch (m) {
 #define RP_GPREP(M)                                                                                            \
   case M:                                                                                                      \

@@ -170,10 +170,11 @@ __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int6
 
 // Same computation with the X rows streamed into shared memory by bulk copies (8 KB row segments,
 // an 8-deep ring completed on mbarriers): the register-resident version keeps only four loads per
-// thread in flight and runs at ~2.3 TB/s, latency-bound. Requires 16-byte aligned X row segments
-// (ldx and d even, X 16-byte aligned).
+// thread in flight and runs at ~2.3 TB/s, latency-bound. The Y row rides in the same stage.
+// Requires 16-byte aligned rows (ldx, d, ldy and m even; X and Y 16-byte aligned).
 constexpr int OZ_GP_STAGES = 8;
-constexpr size_t OZ_GP_SMEM = sizeof(double) * OZ_GP_STAGES * 1024 + 2 * OZ_GP_STAGES * sizeof(uint64_t);
+constexpr int OZ_GP_ROW = 1024 + 16;  // per stage: the X row segment, then the Y row (m <= 16)
+constexpr size_t OZ_GP_SMEM = sizeof(double) * OZ_GP_STAGES * OZ_GP_ROW + 2 * OZ_GP_STAGES * sizeof(uint64_t);
 
 template <int MT>
 __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X, int64_t ldx, int64_t rows, int d,
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
                                                                 double* Cp, double* Mp, int mp, int* E, double* C) {
   constexpr int MM = MT > 0 ? MT : 1;
   extern __shared__ __align__(16) double gp_smem[];
-  double* sx = gp_smem;  // [stage][1024]
-  uint64_t* full = reinterpret_cast<uint64_t*>(gp_smem + OZ_GP_STAGES * 1024);
+  double* sx = gp_smem;  // [stage][OZ_GP_ROW]
+  uint64_t* full = reinterpret_cast<uint64_t*>(gp_smem + OZ_GP_STAGES * OZ_GP_ROW);
   uint64_t* empty = full + OZ_GP_STAGES;
   const int b = blockIdx.z, ch = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const int c0 = blockIdx.x * 1024, i0 = c0 + tid;
@@ -202,8 +203,9 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
     if (tid == 0 && rr < nr) {
       const int st = (int)(rr % OZ_GP_STAGES);
       if (rr >= OZ_GP_STAGES) mbar_wait(&empty[st], (uint32_t)(((rr / OZ_GP_STAGES) + 1) & 1));
-      mbar_arrive_expect_tx(&full[st], (uint32_t)(width * 8));
-      bulk_g2s(sx + st * 1024, xseg + (r0 + rr) * ldx, (uint32_t)(width * 8), &full[st]);
+      mbar_arrive_expect_tx(&full[st], (uint32_t)((width + m) * 8));
+      bulk_g2s(sx + st * OZ_GP_ROW, xseg + (r0 + rr) * ldx, (uint32_t)(width * 8), &full[st]);
+      bulk_g2s(sx + st * OZ_GP_ROW + 1024, y + (r0 + rr) * ldy, (uint32_t)(m * 8), &full[st]);
     }
   };
   for (int s2 = 0; s2 < OZ_GP_STAGES - 1; ++s2) issue(s2);
@@ -217,11 +219,11 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
   for (int64_t rr = 0; rr < nr; ++rr) {
     issue(rr + OZ_GP_STAGES - 1);
     const int st = (int)(rr % OZ_GP_STAGES);
+    mbar_wait(&full[st], (uint32_t)((rr / OZ_GP_STAGES) & 1));
+    const double* xr = sx + st * OZ_GP_ROW;
     double yv[MM];
 #pragma unroll
-    for (int o = 0; o < MM; ++o) yv[o] = (o < m) ? __ldg(y + (r0 + rr) * ldy + o) : 0.0;
-    mbar_wait(&full[st], (uint32_t)((rr / OZ_GP_STAGES) & 1));
-    const double* xr = sx + st * 1024;
+    for (int o = 0; o < MM; ++o) yv[o] = (o < m) ? xr[1024 + o] : 0.0;  // broadcast shared-memory reads
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (tid + 256 * j < width) {
