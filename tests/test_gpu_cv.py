@@ -201,3 +201,17 @@ def test_rank_view_is_bit_identical_to_the_full_sweep(gpu, world):
 
         curves, _, _ = eng.sweep(dX, dY, lams, P, V, ts * grid + tsh, exchange_grams=exchange)
         assert np.array_equal(curves.cpu().numpy(), curves_full[sh.local_folds]), (world, rank)
+
+
+def test_wide_outputs_on_the_tensor_core_paths_match_oracle(gpu):
+    """m = 20 outputs at d = 256: the tensor-core Gram (X^T Y then on the FP64 GEMM: m > 16),
+    two right-hand-side groups in the solve and the CTA-pair hold-out, against the oracle."""
+    n, d, m, k, q, s, r = 1200, 256, 20, 4, 11, 4, 2
+    X, Y = configs.powerlaw(n, d, m, seed=21)
+    grid = orc.make_grid(1e-3, 1e1, q)
+    lams, V, _, ts, tsh, P = pichol.fit_basis(grid[orc.sample_indices(q, s)], r)
+    eng = PicholEngine([n // k] * k, d, m, q, s, r)
+    curves, mean, best = eng.sweep(_dev.to_dev(X), _dev.to_dev(Y), lams, P, V, ts * grid + tsh)
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(n, k), k, grid, g=s, r=r)
+    assert rel(curves.cpu().numpy(), ref["curves"]) <= 1e-8
+    assert np.array_equal(best.cpu().numpy(), ref["best"])
