@@ -159,7 +159,10 @@ int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_
  *   direct: pred = X_val W (DMMA GEMM) fused with (pred - y)^2 or sign-mismatch
  *           row reduction (RMSE or MISCLASS)
  *   gram:   RMSE only, n_val*MSE = y^T y - 2 w^T C_f + w^T G_f w with G_f, C_f
- *           the fold's own Gram blocks (G_f must be symmetrized)
+ *           the fold's own Gram blocks. Only G_f's lower triangle is read
+ *           (w^T G w = 2 w^T T w, T = strict_lower(G) + diag(G)/2); the full-product
+ *           fallback (RP_HOLDOUT_FULL=1, RP_GEMM_WS=0 or W not 16-byte aligned)
+ *           fills G_f's upper triangle in place first.
  * Xval rows of fold f start at Xval + f*fold_stride_rows*ldx (same for Yval).
  * curves: nf x q x m.  work: rp_holdout_workspace_size bytes.               */
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf);
@@ -167,7 +170,7 @@ int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows,
                       const double* Yval, int64_t ldy, int m, const double* W, int64_t ldw,
                       int64_t w_fold_stride, int q, int nf, int metric, double* curves, void* work,
                       void* stream);
-int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
+int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
                     int64_t n_val, int d, int m, const double* W, int64_t ldw, int64_t w_fold_stride, int q,
                     int nf, double* curves, void* work, void* stream);
 

@@ -1088,7 +1088,7 @@ int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows,
   return RP_OK;
 }
 
-int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
+int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
                     int64_t n_val, int d, int m, const double* W, int64_t ldw, int64_t w_fold_stride, int q, int nf,
                     double* curves, void* work, void* stream) {
   RP_REQUIRE(n_val >= 1, "rp_holdout_gram: empty validation set");
@@ -1129,6 +1129,12 @@ int rp_holdout_gram(const double* Gf, int64_t g_stride, const double* Cf, int64_
   // w^T G w = 2 w^T T w with T = strict_lower(G) + diag(G)/2: half the GEMM, only G's lower
   // triangle read (RP_HOLDOUT_FULL=1 forces the full product)
   a.tri_a = (gemm_vec2(a, A_KMAJOR) && g_use_ws && !g_holdout_full) ? 1 : 0;
+  if (!a.tri_a) {  // the full product reads both triangles: fill G_f's upper triangle first
+    const int nt = (d + 31) / 32;
+    const int nmat = g_stride == 0 ? 1 : nf;
+    symmetrize_kernel<<<dim3(nt * (nt + 1) / 2, nmat), dim3(32, 8), 0, st>>>(Gf, d, g_stride);
+    RP_LAUNCH_CHECK("holdout symmetrize");
+  }
   int rc;
   {
     ProfScope prof("holdout_gemm", st);

@@ -174,11 +174,6 @@ class PicholEngine:
         call("rp_fold_systems", ptr(self.G), ptr(self.C), nb, self.d, self.m, _lib.host_ptr(folds), i1 - i0,
              _lib.host_ptr(lams), self.s, ptr(self.A[i0]), ptr(self.rhs[i0]), stream())
 
-    def symmetrize_holdout_blocks(self):
-        if self.holdout == "gram":
-            for f in self.local_folds:
-                call("rp_symmetrize", ptr(self.G[f]), self.d, self.d * self.d, 1, stream())
-
     def stage_factorize(self, part=None, ws=None):
         i0, i1 = part if part is not None else (0, self.nf)
         d = self.d
@@ -273,7 +268,6 @@ class PicholEngine:
         if exchange_grams is not None:
             exchange_grams(self)
         self.stage_systems(sample_lams)
-        self.symmetrize_holdout_blocks()
         mark("assemble")
         self.stage_factorize()
         mark("factorize")

@@ -57,8 +57,6 @@ class ExactEvaluator:
             call("rp_gram_blocks", ptr(self.dX[off:]), d, rows, 1, d, ptr(self.dY[off:]), m, m, ptr(self.G[b]),
                  ptr(self.C[b]), ptr(ws_gram), st)
             call("rp_col_sumsq", ptr(self.dY[off:]), m, rows, 1, m, ptr(self.yy[b]), st)
-        if holdout == "gram":
-            call("rp_symmetrize", ptr(self.G), d, d * d, k, st)
         self.groups = [(c, min(c + MAX_M_PER_SOLVE, m)) for c in range(0, m, MAX_M_PER_SOLVE)]
         self._torch = torch
 
