@@ -100,7 +100,7 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
  * dpotrf (linalg.py:98) for the s sampled lambdas of every local fold.
  * info[b] = 0 on success, j+1 when the leading minor of order j+1 is not
  * positive definite (LAPACK convention).  work: rp_potrf_workspace_size bytes
- * (16-byte aligned). Outer panels of 1536 columns, 128-column blocks factored
+ * (16-byte aligned). Outer panels of 768 columns, 128-column blocks factored
  * left-looking on FP64 DMMA; the trailing updates A22 -= L21 L21^T run on the
  * int8 tensor cores by the Ozaki scheme (FP64-level accuracy) when d % 128 == 0. */
 size_t rp_potrf_workspace_size(int d, int batch);
@@ -108,6 +108,7 @@ size_t rp_potrf_workspace_size(int d, int batch);
 /* Path selection for A/B runs and tests (process-wide; workspace sizes follow it):
  *   "chol_ozaki" 0: Cholesky trailing updates on FP64 DMMA (default 1: int8 tensor cores)
  *   "gram_dmma"  1: Gram blocks on FP64 DMMA even with a workspace (default 0)
+ *   "holdout_ozaki" 0: Gram-form hold-out on FP64 DMMA (default 1: int8 tensor cores)
  *   "profile"    1: time selected kernels with CUDA events (bench roofline)    */
 int rp_set_option(const char* name, int value);
 
