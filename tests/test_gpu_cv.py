@@ -215,3 +215,17 @@ def test_wide_outputs_on_the_tensor_core_paths_match_oracle(gpu):
     ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(n, k), k, grid, g=s, r=r)
     assert rel(curves.cpu().numpy(), ref["curves"]) <= 1e-8
     assert np.array_equal(best.cpu().numpy(), ref["best"])
+
+
+@pytest.mark.parametrize("name,n,d", [("c3", 9000, 1024), ("c4", 12000, 1152)])
+def test_scaled_configs_on_every_tensor_core_path_match_oracle(gpu, name, n, d):
+    """c3 (maclaurin features, k = 5) and c4 (power-law, k = 8) at d > the Cholesky panel width, so
+    every int8 tensor-core path runs: Gram (CTA pairs, one pass for exponents + X^T Y), a trailing
+    update (d = 1152: 384 rows, an odd number of 128-row tiles), the CTA-pair hold-out."""
+    cfg = configs.CONFIGS[name].scaled(n=n, d=d, q=40)
+    X, Y = configs.generate(cfg)
+    curves, mean, best, grid = run_engine(cfg, X, Y, "gram")
+    lam_idx = np.array([0, 13, 27, 39])
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(cfg.n, cfg.k), cfg.k, grid, g=cfg.s, r=cfg.r,
+                                 folds=[0, cfg.k - 1], lam_idx=lam_idx)
+    assert rel(curves[[0, cfg.k - 1]][:, lam_idx], ref["curves"]) <= 1e-8
