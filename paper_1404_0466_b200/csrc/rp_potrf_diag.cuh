@@ -29,7 +29,7 @@ RP_DEVINL void pd_factor_step(double (&row)[16], int ri, int& bad, double* rinv)
   double ajj = __shfl_sync(0xffffffffu, row[J], J);
   if (!bad && !(ajj > 0.0)) bad = J + 1;  // uniform across the warp
   if (bad) ajj = 1.0;                       // keep the (discarded) arithmetic finite
-  const double ljj = sqrt(ajj), rl = 1.0 / ljj;
+  const double ljj = sqrt(ajj), rl = __drcp_rn(ljj);  // = 1.0 / ljj (correctly rounded), no division path
   if (ri > J) row[J] *= rl;
   if (ri == J) row[J] = ljj;
   if ((threadIdx.x & 31) == 0) rinv[J] = rl;
