@@ -53,6 +53,9 @@ int rp_version(void);
 const char* rp_last_error(void);
 /* Number of kernels this library has launched in the process (evidence for bench.py). */
 long long rp_launch_count(void);
+/* Number of tensor-core (Ozaki) products whose device-side range guard tripped, so that the gated
+ * FP64 DMMA fallback computed them, since the library was loaded (synchronizes the device). */
+long long rp_ozaki_fallbacks(void);
 
 /* Number of 64 x 64 tiles of the packed lower triangle of order d, and the
  * size in doubles of one fold's coefficient buffer (both tile copies). */
@@ -71,7 +74,10 @@ int64_t rp_theta_size(int d, int r);
  *      aligned), or NULL. With a workspace and d % 128 == 0, G is computed on
  *      the int8 tensor cores (tcgen05, CTA pairs) by the Ozaki scheme with 7
  *      balanced base-256 digits per value -- FP64-level accuracy (~1e-15
- *      relative to sqrt(G_ii G_jj)), NaN/inf propagated; otherwise by FP64
+ *      relative to sqrt(G_ii G_jj)), NaN/inf propagated -- unless a column of X
+ *      fails the device-side range guard (max |x| > 1024 rms(x): the truncation
+ *      error would exceed FP64's by ~500x), in which case the same call computes G
+ *      by FP64 DMMA (a gated kernel, no host synchronization); otherwise by FP64
  *      DMMA. C is computed by the same FP64 kernel on either path.   */
 size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks);
 int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nblocks, int d,
@@ -102,7 +108,8 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
  * positive definite (LAPACK convention).  work: rp_potrf_workspace_size bytes
  * (16-byte aligned). Outer panels of 768 columns, 128-column blocks factored
  * left-looking on FP64 DMMA; the trailing updates A22 -= L21 L21^T run on the
- * int8 tensor cores by the Ozaki scheme (FP64-level accuracy) when d % 128 == 0. */
+ * int8 tensor cores by the Ozaki scheme (FP64-level accuracy, same range guard
+ * and gated FP64 fallback as rp_gram_blocks) when d % 128 == 0. */
 size_t rp_potrf_workspace_size(int d, int batch);
 
 /* Path selection for A/B runs and tests (process-wide; workspace sizes follow it):
@@ -161,11 +168,16 @@ int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_
  *           row reduction (RMSE or MISCLASS)
  *   gram:   RMSE only, n_val*MSE = y^T y - 2 w^T C_f + w^T G_f w with G_f, C_f
  *           the fold's own Gram blocks. Only G_f's lower triangle is read
- *           (w^T G w = 2 w^T T w, T = strict_lower(G) + diag(G)/2); the full-product
- *           fallback (RP_HOLDOUT_FULL=1, RP_GEMM_WS=0 or W not 16-byte aligned)
- *           fills G_f's upper triangle in place first.
+ *           (w^T G w = 2 w^T T w, T = strict_lower(G) + diag(G)/2) when G_f and W
+ *           are 16-byte aligned with even sizes; otherwise G_f's upper triangle is
+ *           filled in place first and the full product is used. T W runs on the int8
+ *           tensor cores (Ozaki) unless "holdout_ozaki" is 0 or the operands fail the
+ *           range guard (then FP64 DMMA). Columns whose Gram-form value would lose
+ *           more than 20 bits to cancellation (y^T y + |2 w^T c| + w^T G w > 2^20 sse,
+ *           a near-exact fit) are recomputed from the direct residual when Xval is
+ *           given (Xval rows of fold f at Xval + f*fold_stride_rows*ldx, Y likewise).
  * Xval rows of fold f start at Xval + f*fold_stride_rows*ldx (same for Yval).
- * curves: nf x q x m.  work: rp_holdout_workspace_size bytes.               */
+ * curves: nf x q x m.  work: rp_holdout_workspace_size bytes (16-byte aligned). */
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf);
 int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows, int64_t n_val, int d,
                       const double* Yval, int64_t ldy, int m, const double* W, int64_t ldw,
@@ -173,7 +185,8 @@ int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows,
                       void* stream);
 int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
                     int64_t n_val, int d, int m, const double* W, int64_t ldw, int64_t w_fold_stride, int q,
-                    int nf, double* curves, void* work, void* stream);
+                    int nf, const double* Xval, int64_t ldx, int64_t fold_stride_rows, const double* Yval,
+                    int64_t ldy, double* curves, void* work, void* stream);
 
 /* Fold mean + selection (cvsearch._merge, cvsearch.py:154-175): mean[j][o] =
  * (sum_f curves[f][j][o]) / k in fold order; best[o] = first argmin over j

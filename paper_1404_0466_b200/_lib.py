@@ -33,6 +33,7 @@ SIGNATURES = {
     "rp_version": (_i, []),
     "rp_last_error": (ctypes.c_char_p, []),
     "rp_launch_count": (ctypes.c_longlong, []),
+    "rp_ozaki_fallbacks": (ctypes.c_longlong, []),
     "rp_tile_count": (_i64, [_i]),
     "rp_theta_size": (_i64, [_i, _i]),
     "rp_gram_workspace_size": (_sz, [_i, _i64, _i]),
@@ -54,7 +55,8 @@ SIGNATURES = {
     "rp_holdout_workspace_size": (_sz, [_i64, _i, _i, _i, _i]),
     "rp_holdout_direct": (_i, [_vp, _i64, _i64, _i64, _i, _vp, _i64, _i, _vp, _i64, _i64, _i, _i, _i, _vp, _vp,
                                _vp]),
-    "rp_holdout_gram": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _i, _i, _vp, _i64, _i64, _i, _i, _vp, _vp, _vp]),
+    "rp_holdout_gram": (_i, [_vp, _i64, _vp, _i64, _vp, _i64, _i, _i, _vp, _i64, _i64, _i, _i, _vp, _i64, _i64, _vp,
+                             _i64, _vp, _vp, _vp]),
     "rp_select": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp]),
 }
 

@@ -33,6 +33,7 @@ int set_error(int code, const char* fmt, ...) {
 }
 
 static std::atomic<long long> g_launches{0};
+extern int g_solve_lam;  // rp_solve.cu
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static bool g_profile = false;
@@ -52,34 +53,16 @@ void prof_push(const char* name, cudaEvent_t a, cudaEvent_t b, cudaStream_t st) 
 
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 
-// RP_POTRF_DIAG=simple selects the unblocked shared-memory diagonal factor (A/B testing).
-static const bool g_simple_diag = [] {
-  const char* e = getenv("RP_POTRF_DIAG");
-  return e && e[0] == 's';
-}();
-
-// RP_GEMM_WS=0 selects the cp.async GEMM everywhere (A/B testing of the two GEMM pipelines).
-static const bool g_use_ws = [] {
-  const char* e = getenv("RP_GEMM_WS");
-  return !(e && e[0] == '0');
-}();
-
-// Gram-form hold-out on the int8 tensor cores (Ozaki, rp_ozaki.cuh oz_holdout) when the
-// workspace allows; rp_set_option("holdout_ozaki", 0) or RP_HOLDOUT_OZAKI=0 keeps FP64 DMMA.
-static bool g_holdout_ozaki = [] {
-  const char* e = getenv("RP_HOLDOUT_OZAKI");
-  return !(e && e[0] == '0');
-}();
-
-static bool g_gram_dmma = [] {
-  const char* e = getenv("RP_GRAM_DMMA");
-  return e && e[0] == '1';
-}();
-
-static const bool g_holdout_full = [] {
-  const char* e = getenv("RP_HOLDOUT_FULL");
-  return e && e[0] == '1';
-}();
+// Path options (rp_set_option; the environment variables set the initial value for A/B runs):
+// Gram-form hold-out on the int8 tensor cores (Ozaki, rp_ozaki.cuh oz_holdout) when the workspace
+// allows ("holdout_ozaki" 0 / RP_HOLDOUT_OZAKI=0 keeps FP64 DMMA); Gram blocks on FP64 DMMA even
+// with a workspace ("gram_dmma" 1 / RP_GRAM_DMMA=1).
+static bool env_flag(const char* name, bool dflt) {
+  const char* e = getenv(name);
+  return e ? e[0] == '1' : dflt;
+}
+static bool g_holdout_ozaki = env_flag("RP_HOLDOUT_OZAKI", true);
+static bool g_gram_dmma = env_flag("RP_GRAM_DMMA", false);
 
 // ------------------------------------------------------------------ GEMM dispatch
 
@@ -93,13 +76,13 @@ template <int AL, int BM, int BN, int WM, int WN, int EPI>
 static int gemm(const GemmArgs& a, int batch, cudaStream_t st, const char* name) {
   if (a.M <= 0 || a.N <= 0 || batch <= 0) return RP_OK;
   bool vec2 = gemm_vec2(a, AL);
-  if (a.tri_a && !(vec2 && g_use_ws)) return set_error(RP_EINVAL, "%s: triangular A needs the bulk-copy GEMM", name);
+  if (a.tri_a && !vec2) return set_error(RP_EINVAL, "%s: triangular A needs the bulk-copy GEMM", name);
   const int mt = (a.M + BM - 1) / BM, nt = (a.N + BN - 1) / BN;
   if (a.lower_only && (BM != BN || a.M != a.N)) return set_error(RP_EINVAL, "%s: lower_only needs square", name);
   dim3 grid(a.lower_only ? mt * (mt + 1) / 2 : mt * nt, batch);
   size_t smem = GemmSmem<AL, BM, BN>::BYTES;
   // bulk-copy (warp-specialised) path: every copied tile row must be 16-byte aligned and sized
-  const bool ws = vec2 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0) && g_use_ws;
+  const bool ws = vec2 && a.N % 2 == 0 && (AL == A_KMAJOR ? a.M % 2 == 0 : a.K % 2 == 0);
   if (ws) {
     auto k = dgemm_ws_kernel<AL, BM, BN, WM, WN, EPI>;
     size_t wsm = WsSmem<AL, BM, BN>::BYTES;
@@ -241,74 +224,6 @@ static int CHOL_OB = [] {
   int v = e ? atoi(e) : 768;
   return v >= 128 && v % 128 == 0 ? v : 768;
 }();
-
-// Factor the NB x NB diagonal block at (k0, k0) of every batch matrix in shared memory
-// (unblocked right-looking, LAPACK dpotf2 order: sqrt pivot, scale by reciprocal, rank-1 update),
-// write L11 back, and write inv(L11) (column-major NB x NB, zero above the diagonal) to `inv`
-// for the panel TRSM, which then runs as a DMMA GEMM.
-__global__ void __launch_bounds__(1024) potrf_diag_kernel(double* A, int d, int64_t stride, int k0, double* inv,
-                                                          int* info) {
-  constexpr int NB = CHOL_NB;
-  extern __shared__ double a[];  // NB*NB column-major
-  const int b = blockIdx.x, tid = threadIdx.x;
-  if (info[b] != 0) return;
-  double* Ab = A + b * stride;
-  const int nbv = min(NB, d - k0);
-  for (int e = tid; e < NB * NB; e += 1024) {
-    int i = e % NB, j = e / NB;
-    double v;
-    if (i < nbv && j < nbv) v = (i >= j) ? Ab[(int64_t)(k0 + j) * d + k0 + i] : 0.0;
-    else v = (i == j) ? 1.0 : 0.0;
-    a[e] = v;
-  }
-  __syncthreads();
-  for (int j = 0; j < nbv; ++j) {
-    const double ajj = a[j * NB + j];
-    if (!(ajj > 0.0)) {
-      if (tid == 0) info[b] = k0 + j + 1;
-      return;
-    }
-    const double ljj = sqrt(ajj);
-    const double rl = 1.0 / ljj;
-    for (int i = j + 1 + tid; i < nbv; i += 1024) a[j * NB + i] *= rl;
-    __syncthreads();
-    if (tid == 0) a[j * NB + j] = ljj;
-    const int n1 = nbv - j - 1;
-    for (int e = tid; e < n1 * n1; e += 1024) {
-      const int c = e / n1, i = e - c * n1;
-      if (i >= c) a[(j + 1 + c) * NB + j + 1 + i] -= a[j * NB + j + 1 + i] * a[j * NB + j + 1 + c];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < NB * NB; e += 1024) {
-    int i = e % NB, j = e / NB;
-    if (i < nbv && j < nbv && i >= j) Ab[(int64_t)(k0 + j) * d + k0 + i] = a[e];
-  }
-  // inv(L11): warp w solves columns c = w, w+32, ...; lane owns rows lane + 32 r.
-  double* X = inv + (int64_t)b * NB * NB;
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int c = warp; c < nbv; c += 32) {
-    double acc[NB / 32];
-#pragma unroll
-    for (int r = 0; r < NB / 32; ++r) acc[r] = 0.0;
-    for (int k = lane; k < c; k += 32) X[(int64_t)c * NB + k] = 0.0;
-    for (int k = c; k < nbv; ++k) {
-      const int owner = k & 31, rk = k >> 5;
-      double mine = 0.0;
-#pragma unroll
-      for (int r = 0; r < NB / 32; ++r)
-        if (r == rk) mine = acc[r];
-      double xk = ((k == c ? 1.0 : 0.0) - mine) / a[k * NB + k];
-      xk = __shfl_sync(0xffffffffu, xk, owner);
-      if (lane == owner) X[(int64_t)c * NB + k] = xk;
-#pragma unroll
-      for (int r = 0; r < NB / 32; ++r) {
-        const int i = lane + 32 * r;
-        if (i > k && i < nbv) acc[r] = fma(a[k * NB + i], xk, acc[r]);
-      }
-    }
-  }
-}
 
 // ------------------------------------------------------------------ fit
 
@@ -468,8 +383,14 @@ __global__ void import_kernel(const double* vec, int d, int P, const int64_t* pe
 // ------------------------------------------------------------------ hold-out reductions
 
 // sse[f][n] = sum_tm partial[f][tm][n] (fixed order), then curves[f][j][o] from it.
+// Gram form: n_val * MSE = y^T y - 2 w^T c + w^T G w loses log2((y^T y + |2 w^T c| + w^T G w) / sse)
+// bits to cancellation (a near-exact fit, tiny noise). Columns that would lose more than 20 bits
+// (relative error above ~1e-10 on the RMSE) are listed in rep_list and recomputed from the direct
+// residual by holdout_repair_kernel (cvsearch.py:119-120's arithmetic).
+constexpr double HOLDOUT_CANCEL = 1048576.0;  // 2^20
 __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, int m, int64_t n_val, int metric,
-                                      const double* yy, const double* bc, double quad_scale, double* curves) {
+                                      const double* yy, const double* bc, double quad_scale, double* curves,
+                                      int* rep_count, int* rep_list) {
   const int f = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -478,7 +399,10 @@ __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, 
   double out;
   if (yy) {  // Gram form: n_val * MSE = y^T y - 2 w^T c + w^T G w
     const int o = n % m;
-    double sse = yy[f * m + o] - 2.0 * bc[(int64_t)f * N + n] + quad_scale * s;
+    const double yv = yy[f * m + o], b2 = 2.0 * bc[(int64_t)f * N + n], qd = quad_scale * s;
+    double sse = yv - b2 + qd;
+    if (rep_list != nullptr && !(sse * HOLDOUT_CANCEL >= fabs(yv) + fabs(b2) + fabs(qd)))
+      rep_list[atomicAdd(rep_count, 1)] = f * N + n;
     out = sqrt((sse > 0.0 ? sse : 0.0) / (double)n_val);
   } else if (metric == RP_METRIC_RMSE) {
     out = sqrt(s / (double)n_val);
@@ -486,6 +410,57 @@ __global__ void holdout_finish_kernel(const double* partial, int mtiles, int N, 
     out = s / (double)n_val;
   }
   curves[(int64_t)f * N + n] = out;
+}
+
+// Direct residual of the listed Gram-form columns: part[c][chunk] = sum over the chunk's rows of
+// (x_row . w - y_row)^2 (rows in order per warp, warps combined in order: deterministic for a
+// column whatever its position in the list). w is staged in shared memory when it fits.
+constexpr int REP_CHUNKS = 16;
+__global__ void __launch_bounds__(256) holdout_repair_kernel(const double* X, int64_t ldx, int64_t fold_stride_rows,
+                                                             int64_t n_val, int d, const double* Y, int64_t ldy, int m,
+                                                             const double* W, int64_t ldw, int64_t w_fold_stride,
+                                                             int N, const int* rep_count, const int* rep_list,
+                                                             int w_in_smem, double* part) {
+  extern __shared__ double rep_w[];
+  __shared__ double red[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int count = *rep_count;
+  const int64_t r0 = n_val * blockIdx.x / REP_CHUNKS, r1 = n_val * (blockIdx.x + 1) / REP_CHUNKS;
+  for (int c = blockIdx.y; c < count; c += gridDim.y) {
+    const int id = rep_list[c], f = id / N, n = id - f * N, o = n % m;
+    const double* w = W + f * w_fold_stride + n;
+    if (w_in_smem)
+      for (int k = threadIdx.x; k < d; k += 256) rep_w[k] = w[(int64_t)k * ldw];
+    __syncthreads();
+    double acc = 0.0;  // lane 0: this warp's rows
+    for (int64_t r = r0 + warp; r < r1; r += 8) {
+      const double* x = X + (f * fold_stride_rows + r) * ldx;
+      double p = 0.0;
+      for (int k = lane; k < d; k += 32) p = fma(x[k], w_in_smem ? rep_w[k] : w[(int64_t)k * ldw], p);
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) p += __shfl_xor_sync(0xffffffffu, p, sh);
+      const double e = p - Y[(f * fold_stride_rows + r) * ldy + o];
+      acc = fma(e, e, acc);
+    }
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < 8; ++i) t += red[i];
+      part[(int64_t)c * REP_CHUNKS + blockIdx.x] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void holdout_repair_finish_kernel(const int* rep_count, const int* rep_list, const double* part,
+                                             int64_t n_val, double* curves) {
+  const int count = *rep_count;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < count; c += gridDim.x * blockDim.x) {
+    double sse = 0.0;
+    for (int i = 0; i < REP_CHUNKS; ++i) sse += part[(int64_t)c * REP_CHUNKS + i];
+    curves[rep_list[c]] = sqrt(sse / (double)n_val);
+  }
 }
 
 // bc[f][n] = sum_i W[i][n] * C_f[i][o]
@@ -548,10 +523,11 @@ __global__ void select_kernel(const double* curves, int k, int q, int m, double*
 // the row-chunk count depends on it). scratch: nscratch bytes for the chunk partials (the Gram
 // workspace's slice area, overwritten by the slicing afterwards), or nullptr for one chunk.
 static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, int d, const double* Y, int64_t ldy,
-                     int m, int* E, int mp, double* C, void* scratch, size_t nscratch, cudaStream_t st) {
+                     int m, int* E, int mp, double* C, int* guard, void* scratch, size_t nscratch, cudaStream_t st) {
   RP_REQUIRE(m >= 1 && m <= 16, "gram prep: m=%d outside [1, 16]", m);
-  // row chunks: ~4 waves of 1024-column CTAs, as many as the scratch holds
-  const size_t per_chunk = sizeof(double) * (size_t)nblocks * (m + 1) * d;
+  // row chunks: ~4 waves of 1024-column CTAs, as many as the scratch holds (per chunk: the m
+  // partial sums, the column maxima, exponent sums and nonzero counts of the range guard)
+  const size_t per_chunk = sizeof(double) * (size_t)nblocks * (m + 3) * d;
   int nchunk = 32;
   if (rows < 256) nchunk = 1;
   while (nchunk > 1 && (scratch == nullptr || per_chunk * nchunk > nscratch || rows / nchunk < 64)) nchunk /= 2;
@@ -568,9 +544,9 @@ static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, in
       cudaFuncSetAttribute(oz_gram_prep_bulk_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
                            (int)OZ_GP_SMEM);                                                                   \
       oz_gram_prep_bulk_kernel<M><<<grid, 256, OZ_GP_SMEM, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, \
-                                                                 E, C);                                        \
+                                                                 E, C, guard);                                      \
     } else {                                                                                                   \
-      oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, E, C);     \
+      oz_gram_prep_kernel<M><<<grid, 256, 0, st>>>(X, ldx, rows, d, Y, ldy, m, nchunk, Cp, Mp, mp, E, C, guard); \
     }                                                                                                          \
     break;
     RP_GPREP(1) RP_GPREP(2) RP_GPREP(3) RP_GPREP(4) RP_GPREP(5) RP_GPREP(6) RP_GPREP(7) RP_GPREP(8)
@@ -579,16 +555,12 @@ static int gram_prep(const double* X, int64_t ldx, int64_t rows, int nblocks, in
   }
   RP_LAUNCH_CHECK("gram prep");
   if (nchunk > 1) {
-    oz_gram_prep_reduce_kernel<<<dim3((mp + 255) / 256, nblocks), 256, 0, st>>>(Cp, Mp, d, m, nchunk, mp, E, C);
+    oz_gram_prep_reduce_kernel<<<dim3((mp + 255) / 256, nblocks), 256, 0, st>>>(Cp, Mp, d, m, nchunk, mp, E, C,
+                                                                              nblocks, guard);
     RP_LAUNCH_CHECK("gram prep reduce");
   }
   return RP_OK;
 }
-
-static const bool g_xty_gemm = [] {
-  const char* e = getenv("RP_XTY_GEMM");
-  return e && e[0] == '1';
-}();
 
 }  // namespace rp
 
@@ -603,6 +575,12 @@ int rp_version(void) { return 1; }
 long long rp_launch_count(void) { return rp::g_launches.load(); }
 
 const char* rp_last_error(void) { return rp::g_last_error.c_str(); }
+
+long long rp_ozaki_fallbacks(void) {
+  unsigned long long v = 0;
+  if (cudaMemcpyFromSymbol(&v, g_oz_fallbacks, sizeof(v)) != cudaSuccess) return -1;
+  return (long long)v;
+}
 
 int64_t rp_tile_count(int d) {
   int64_t nt = (d + 63) / 64;
@@ -650,7 +628,7 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   RP_REQUIRE(rows_per_block <= 0x7fffffff, "rp_gram_blocks: block too tall");
   RP_REQUIRE(work == nullptr || ((uintptr_t)work & 15) == 0, "rp_gram_blocks: workspace must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  // Ozaki-scheme tensor-core Gram (int8 tcgen05) when a workspace is given; RP_GRAM_DMMA=1 forces FP64 DMMA
+  // Ozaki-scheme tensor-core Gram (int8 tcgen05) when a workspace is given ("gram_dmma" forces FP64 DMMA)
   const bool ozaki = work != nullptr && !g_gram_dmma && oz_supported(d, rows_per_block, nblocks);
   GemmArgs a = gemm_args();
   a.M = a.N = d;
@@ -664,50 +642,54 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
   a.lower_only = 1;
   const bool want_c = m > 0 && C != nullptr;
   if (want_c) RP_REQUIRE(Y != nullptr && ldy >= m, "rp_gram_blocks: Y");
-  // tensor-core path with C wanted: one fused pass computes the slicing exponents and X^T Y
-  const bool fused = ozaki && want_c && m <= 16 && !g_xty_gemm && oz_pair_enabled();
-  const bool side = !fused && want_c && m <= 16 && !g_xty_gemm;
-  cudaStream_t xs = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-  if (side) {
-    SideStreams* ss = side_streams(st, 0);
-    xs = ss->s[0];
-    fork = ss->fork;
-    join = ss->join[0];
-  }
-  if (side) {  // the side stream starts from the same point of `st` as the SYRK
-    cudaError_t e = cudaEventRecord(fork, st);
-    if (e != cudaSuccess) return cuda_status(e, "gram fork");
-    cudaStreamWaitEvent(xs, fork, 0);
-  }
+  // C_b = X_b^T Y_b by the one-pass prep kernel (m <= 16), on either Gram path with the same row
+  // chunking (the same scratch), so C is bit-identical whichever path computes G
+  const bool prep_c = want_c && m <= 16;
+  const size_t ws = work ? rp_gram_workspace_size(d, rows_per_block, nblocks) : 0;
+  const size_t eb = OZ_HDR + oz_eb(oz_mp(d), nblocks);
+  void* scratch = work ? reinterpret_cast<uint8_t*>(work) + eb : nullptr;
+  const size_t nscratch = work ? ws - eb : 0;
   // X_b row-major (rows x d) is the column-major d x rows matrix A_b with lda = ldx: G_b = A_b A_b^T
   const OzIn oin{X, ldx, rows_per_block * ldx, rows_per_block, d, nblocks};
-  if (fused) {
-    // one pass over X for the row exponents of the slicing and C_b = X_b^T Y_b, then the SYRK
-    {
+  int rc;
+  if (ozaki) {
+    int* guard = oz_guard_of(work);
+    if (prep_c) {
+      // one pass over X for the row exponents (+ range guard) of the slicing and C_b = X_b^T Y_b
       ProfScope prof("gram_prep", st);
-      const size_t eb = oz_eb(oz_mp(d), nblocks);
-      const size_t ws = rp_gram_workspace_size(d, rows_per_block, nblocks);
-      int rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, reinterpret_cast<int*>(work), oz_mp(d), C,
-                         reinterpret_cast<uint8_t*>(work) + eb, ws - eb, st);
+      cudaError_t e = cudaMemsetAsync(guard, 0, sizeof(int), st);
+      if (e != cudaSuccess) return cuda_status(e, "gram guard");
+      rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m,
+                     reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(work) + OZ_HDR), oz_mp(d), C, guard, scratch,
+                     nscratch, st);
       if (rc) return rc;
     }
-    return oz_syrk(oin, G, d, (int64_t)d * d, false, work, st, "oz_syrk", true);
-  }
-  int rc = ozaki ? oz_syrk(oin, G, d, (int64_t)d * d, false, work, st)
-                 : gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
-  if (rc) return rc;
-  if (side) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
-    const size_t eb = work ? oz_eb(oz_mp(d), nblocks) : 0;
-    const size_t ws = work ? rp_gram_workspace_size(d, rows_per_block, nblocks) : 0;
-    rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, nullptr, d, C,
-                   work ? reinterpret_cast<uint8_t*>(work) + eb : nullptr, ws - eb, xs);
+    rc = oz_syrk(oin, G, d, (int64_t)d * d, false, work, st, "oz_syrk", prep_c);
     if (rc) return rc;
-    cudaEventRecord(join, xs);
-    cudaStreamWaitEvent(st, join, 0);
-    return RP_OK;
+    a.run_if_set = guard;  // FP64 fallback when a block is outside the Ozaki range
+    rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk (guarded fallback)");
+    if (rc) return rc;
+  } else {
+    cudaStream_t xs = nullptr;
+    cudaEvent_t join = nullptr;
+    if (prep_c) {  // X^T Y on a side stream that starts from the same point of `st` as the SYRK
+      SideStreams* ss = side_streams(st, 0);
+      xs = ss->s[0];
+      join = ss->join[0];
+      cudaError_t e = cudaEventRecord(ss->fork, st);
+      if (e != cudaSuccess) return cuda_status(e, "gram fork");
+      cudaStreamWaitEvent(xs, ss->fork, 0);
+    }
+    rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(a, nblocks, st, "gram syrk");
+    if (rc) return rc;
+    if (prep_c) {  // launched after the SYRK so its CTAs fill in next to the SYRK's; joined on `st`
+      rc = gram_prep(X, ldx, rows_per_block, nblocks, d, Y, ldy, m, nullptr, d, C, nullptr, scratch, nscratch, xs);
+      if (rc) return rc;
+      cudaEventRecord(join, xs);
+      cudaStreamWaitEvent(st, join, 0);
+    }
   }
-  if (want_c) {
+  if (want_c && !prep_c) {
     GemmArgs b = gemm_args();
     b.M = d;
     b.N = m;
@@ -722,8 +704,9 @@ int rp_gram_blocks(const double* X, int64_t ldx, int64_t rows_per_block, int nbl
     b.ldc = d;
     b.strideC = (int64_t)d * m;
     rc = gemm<A_KMAJOR, 128, 16, 16, 16, EPI_STORE>(b, nblocks, st, "gram xty");
+    if (rc) return rc;
   }
-  return rc;
+  return RP_OK;
 }
 
 int rp_symmetrize(double* G, int d, int64_t stride, int nmat, void* stream) {
@@ -781,10 +764,7 @@ static int CHOL_GROUPS = [] {
 // Trailing updates A22 -= L21 L21^T on the int8 tensor cores (Ozaki) instead of FP64 DMMA
 // (measured at c4: factorize 36.2 ms DMMA vs 33.3 ms Ozaki). rp_set_option("chol_ozaki", 0) or
 // RP_CHOL_OZAKI=0 keeps them on DMMA.
-static bool g_chol_ozaki = [] {
-  const char* e = getenv("RP_CHOL_OZAKI");
-  return !(e && e[0] == '0');
-}();
+static bool g_chol_ozaki = env_flag("RP_CHOL_OZAKI", true);
 
 // Per-group slice workspace of the tensor-core trailing update (largest update: d - OB rows).
 static size_t potrf_oz_group_bytes(int d, int batch) {
@@ -798,7 +778,9 @@ static size_t potrf_oz_group_bytes(int d, int batch) {
 size_t rp_potrf_workspace_size(int d, int batch) {
   const size_t inv = ((sizeof(double) * (size_t)batch * CHOL_NB * CHOL_NB) + 1023) / 1024 * 1024;
   const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
-  return inv + (g_chol_ozaki ? (size_t)groups * potrf_oz_group_bytes(d, batch) : 0);
+  // sized for the tensor-core trailing updates whatever "chol_ozaki" is now, so a workspace stays
+  // valid if the option changes between the query and the call
+  return inv + (size_t)groups * potrf_oz_group_bytes(d, batch);
 }
 
 double rp_profile_ms(const char* name) {
@@ -847,6 +829,11 @@ int rp_set_option(const char* name, int value) {
     g_holdout_ozaki = value != 0;
     return RP_OK;
   }
+  if (strcmp(name, "solve_lam") == 0) {
+    RP_REQUIRE(value >= 0 && value <= 16, "rp_set_option: solve_lam %d outside [0, 16]", value);
+    g_solve_lam = value;
+    return RP_OK;
+  }
   if (strcmp(name, "profile") == 0) {
     g_profile = value != 0;
     return RP_OK;
@@ -863,8 +850,6 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
   double* inv = (double*)work;
   cudaError_t e = cudaMemsetAsync(info, 0, sizeof(int) * batch, st);
   if (e != cudaSuccess) return cuda_status(e, "potrf memset");
-  const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
-  cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(potrf_diag_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PD_SMEM);
   const int groups = batch < CHOL_GROUPS ? batch : CHOL_GROUPS;
   // tensor-core trailing updates: one slice workspace per group after inv(L11)
@@ -896,7 +881,6 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
 
 static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, double* inv, void* ozws,
                        cudaStream_t st) {
-  const size_t smem = sizeof(double) * CHOL_NB * CHOL_NB;
   // Two-level blocked right-looking factorization. Outer panels of CHOL_OB columns are factored
   // left-looking in 128-column blocks (update from the panel's earlier blocks as one DMMA GEMM,
   // shared-memory diagonal factor + inverse, panel TRSM as a DMMA GEMM against the inverse);
@@ -924,17 +908,9 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
         int rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_STORE>(u, batch, st, "potrf panel update");
         if (rc) return rc;
       }
-      static const bool skip_diag = [] {  // RP_CHOL_DBG=1 (timing experiments only: wrong factors)
-        const char* e = getenv("RP_CHOL_DBG");
-        return e && e[0] == '1';
-      }();
-      if (!skip_diag) {
+      {
         ProfScope prof("chol_diag", st);
-        if (g_simple_diag) {
-          potrf_diag_kernel<<<batch, 1024, smem, st>>>(A, d, stride, k1, inv, info);
-        } else {
-          potrf_diag_dmma_kernel<<<batch, PD_THREADS, PD_SMEM, st>>>(A, d, stride, k1, inv, info);
-        }
+        potrf_diag_dmma_kernel<<<batch, PD_THREADS, PD_SMEM, st>>>(A, d, stride, k1, inv, info);
         RP_LAUNCH_CHECK("potrf_diag");
       }
       const int rows = d - k1 - nb;
@@ -963,13 +939,14 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
     if (rem <= 0) break;
     // A22 -= L21 L21^T with K = ob (lower tiles)
     const double* L21 = A + (int64_t)k0 * d + k0 + ob;
-    if (ozws && oz_supported(rem, ob, batch)) {  // on the int8 tensor cores (Ozaki scheme)
+    const bool ozaki = ozws && oz_supported(rem, ob, batch);
+    if (ozaki) {  // on the int8 tensor cores (Ozaki scheme), FP64 fallback below gated on its range guard
       const OzIn oin{L21, d, stride, ob, rem, batch};
       int rc = oz_syrk(oin, A + (int64_t)(k0 + ob) * d + k0 + ob, d, stride, true, ozws, st, "oz_syrk_chol");
       if (rc) return rc;
-      continue;
     }
     GemmArgs u = gemm_args();
+    u.run_if_set = ozaki ? oz_guard_of(ozws) : nullptr;
     u.M = u.N = rem;
     u.K = ob;
     u.A = u.B = L21;
@@ -1047,11 +1024,19 @@ static int64_t holdout_mt(int64_t n_val, int d) {
   return mt_direct > mt_gram ? mt_direct : mt_gram;
 }
 
+// Hold-out workspace: [partials nf x mt x N][bc nf x N] [repair: count, list nf x N, partials
+// nf x N x REP_CHUNKS] [Ozaki slices (Gram form on the tensor cores)].
+static size_t holdout_base_bytes(int64_t n_val, int d, int64_t N, int nf) {
+  return (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + nf * N) + 1023) / 1024 * 1024;
+}
+static size_t holdout_rep_bytes(int64_t N, int nf) {
+  return (16 + sizeof(int) * (size_t)nf * N + sizeof(double) * (size_t)nf * N * REP_CHUNKS + 1023) / 1024 * 1024;
+}
+
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf) {
   const int64_t N = (int64_t)q * m;
-  const size_t base = (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + nf * N) + 1023) / 1024 * 1024;
   const bool oz = g_holdout_ozaki && oz_holdout_supported(d, N, nf);
-  return base + (oz ? oz_holdout_workspace(d, N, nf, false) : 0);
+  return holdout_base_bytes(n_val, d, N, nf) + holdout_rep_bytes(N, nf) + (oz ? oz_holdout_workspace(d, N, nf, false) : 0);
 }
 
 int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows, int64_t n_val, int d,
@@ -1083,34 +1068,32 @@ int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows,
   if (rc) return rc;
   const int mtiles = (int)((n_val + 127) / 128);
   holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, metric, nullptr, nullptr,
-                                                             1.0, curves);
+                                                             1.0, curves, nullptr, nullptr);
   RP_LAUNCH_CHECK("holdout finish");
   return RP_OK;
 }
 
 int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_stride, const double* yy,
                     int64_t n_val, int d, int m, const double* W, int64_t ldw, int64_t w_fold_stride, int q, int nf,
+                    const double* Xval, int64_t ldx, int64_t fold_stride_rows, const double* Yval, int64_t ldy,
                     double* curves, void* work, void* stream) {
   RP_REQUIRE(n_val >= 1, "rp_holdout_gram: empty validation set");
+  RP_REQUIRE(((uintptr_t)work & 15) == 0, "rp_holdout_gram: workspace must be 16-byte aligned");
+  RP_REQUIRE(Xval == nullptr || (Yval != nullptr && ldx >= d && ldy >= m), "rp_holdout_gram: Xval / Yval");
   cudaStream_t st = (cudaStream_t)stream;
   const int N = q * m;
   const int mtiles = (d + 127) / 128;
-  double* partial = (double*)work;
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(work);
+  double* partial = reinterpret_cast<double*>(w8);
   double* bc = partial + (size_t)nf * holdout_mt(n_val, d) * N;
-  const size_t base =
-      (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + (int64_t)nf * N) + 1023) / 1024 * 1024;
-  if (g_holdout_ozaki && oz_holdout_supported(d, N, nf) && ((uintptr_t)work & 15) == 0) {
-    // w^T G w = 2 w^T T w on the int8 tensor cores: partials [f][mtiles][N]
-    int rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial,
-                        reinterpret_cast<uint8_t*>(work) + base, st);
-    if (rc) return rc;
-    holdout_bc_kernel<<<dim3((N + 31) / 32, nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
-    RP_LAUNCH_CHECK("holdout bc");
-    holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy,
-                                                               bc, 2.0, curves);
-    RP_LAUNCH_CHECK("holdout gram finish");
-    return RP_OK;
-  }
+  w8 += holdout_base_bytes(n_val, d, N, nf);
+  int* rep_count = reinterpret_cast<int*>(w8);
+  int* rep_list = rep_count + 4;
+  double* rep_part = reinterpret_cast<double*>(w8 + 16 + sizeof(int) * (size_t)nf * N);
+  w8 += holdout_rep_bytes(N, nf);
+  cudaError_t e = cudaMemsetAsync(rep_count, 0, sizeof(int), st);
+  if (e != cudaSuccess) return cuda_status(e, "holdout repair count");
+
   GemmArgs a = gemm_args();
   a.M = d;
   a.N = N;
@@ -1126,16 +1109,21 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
   a.strideY = w_fold_stride;
   a.ycols = N;
   a.partial = partial;
-  // w^T G w = 2 w^T T w with T = strict_lower(G) + diag(G)/2: half the GEMM, only G's lower
-  // triangle read (RP_HOLDOUT_FULL=1 forces the full product)
-  a.tri_a = (gemm_vec2(a, A_KMAJOR) && g_use_ws && !g_holdout_full) ? 1 : 0;
-  if (!a.tri_a) {  // the full product reads both triangles: fill G_f's upper triangle first
+  // w^T G w = 2 w^T T w with T = strict_lower(G) + diag(G)/2: half the GEMM, only G's lower triangle read
+  a.tri_a = gemm_vec2(a, A_KMAJOR) ? 1 : 0;
+  int rc;
+  if (a.tri_a && g_holdout_ozaki && oz_holdout_supported(d, N, nf)) {
+    // T W on the int8 tensor cores (partials [f][mtiles][N]); the DMMA product behind it runs only
+    // when the range guard trips
+    rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial, w8, st);
+    if (rc) return rc;
+    a.run_if_set = oz_guard_of(w8);
+  } else if (!a.tri_a) {  // the full product reads both triangles: fill G_f's upper triangle first
     const int nt = (d + 31) / 32;
     const int nmat = g_stride == 0 ? 1 : nf;
     symmetrize_kernel<<<dim3(nt * (nt + 1) / 2, nmat), dim3(32, 8), 0, st>>>(Gf, d, g_stride);
     RP_LAUNCH_CHECK("holdout symmetrize");
   }
-  int rc;
   {
     ProfScope prof("holdout_gemm", st);
     rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
@@ -1144,8 +1132,21 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
   holdout_bc_kernel<<<dim3((N + 31) / 32, nf), 256, 0, st>>>(W, ldw, w_fold_stride, Cf, c_stride, d, m, N, bc);
   RP_LAUNCH_CHECK("holdout bc");
   holdout_finish_kernel<<<dim3(grid1d(N), nf), 256, 0, st>>>(partial, mtiles, N, m, n_val, RP_METRIC_RMSE, yy, bc,
-                                                             a.tri_a ? 2.0 : 1.0, curves);
+                                                             a.tri_a ? 2.0 : 1.0, curves,
+                                                             Xval ? rep_count : nullptr, rep_list);
   RP_LAUNCH_CHECK("holdout gram finish");
+  if (Xval != nullptr) {  // cancellation repair (no work unless a column was listed)
+    const size_t wsm = sizeof(double) * (size_t)d;
+    const int in_smem = wsm <= 192 * 1024 ? 1 : 0;
+    if (in_smem)
+      cudaFuncSetAttribute(holdout_repair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+    holdout_repair_kernel<<<dim3(REP_CHUNKS, 32), 256, in_smem ? wsm : 0, st>>>(
+        Xval, ldx, fold_stride_rows, n_val, d, Yval, ldy, m, W, ldw, w_fold_stride, N, rep_count, rep_list, in_smem,
+        rep_part);
+    RP_LAUNCH_CHECK("holdout repair");
+    holdout_repair_finish_kernel<<<8, 256, 0, st>>>(rep_count, rep_list, rep_part, n_val, curves);
+    RP_LAUNCH_CHECK("holdout repair finish");
+  }
   return RP_OK;
 }
 

@@ -44,7 +44,14 @@ struct GemmArgs {
   int64_t ldy, strideY;
   int ycols;
   double* partial;  // [batch][mtiles][N]
+  // gated launch (the FP64 fallback of a tensor-core product): when non-null the kernel does its
+  // work only if *run_if_set != 0 (the Ozaki range guard tripped), else every CTA exits at once
+  const int* run_if_set;
 };
+
+// Number of gated FP64 fallbacks that ran (tensor-core products whose range guard tripped);
+// read by rp_ozaki_fallbacks().
+__device__ unsigned long long g_oz_fallbacks = 0;
 
 constexpr int GEMM_BK = 16;
 constexpr int GEMM_STAGES = 3;
@@ -60,6 +67,10 @@ struct GemmSmem {
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI, bool VEC2>
 __global__ void __launch_bounds__(256) dgemm_kernel(GemmArgs p) {
+  if (p.run_if_set != nullptr) {
+    if (*p.run_if_set == 0) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
+  }
   constexpr int BK = GEMM_BK;
   constexpr int MT = WM / 8, NT = WN / 8;
   constexpr int WARPS_M = BM / WM;
@@ -335,6 +346,10 @@ RP_DEVINL void ws_ktile(double (&acc)[MT][NT][2], const double* a_s, const doubl
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
 __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_tiles) {
+  if (p.run_if_set != nullptr) {
+    if (*p.run_if_set == 0) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
+  }
   constexpr int BK = GEMM_BK;
   constexpr int MT = WM / 8, NT = WN / 8;
   constexpr int WARPS_M = BM / WM;

@@ -15,18 +15,21 @@
 // the digit truncation): FP64-level accuracy in the sqrt(C_ii C_jj) norm.
 //
 // Kernels:
-//   oz_rowexp_kernel   E[b][i]                      (one pass over A, row max)
-//   oz_slice_kernel    digits, K-major int8 slices [b][p][i][kpad]
-//   oz_syrk_kernel     persistent, warp-specialised, one 128 x 128 lower tile (I >= J) at a time:
-//                      warp 0 issues the TMA loads (SWIZZLE_32B boxes of 32 k x 128 rows, the
-//                      slices of A_I and A_J a pass needs), warp 1 allocates TMEM and issues the
-//                      tcgen05.mma (M = N = 128, K = 32) into 4 weight-group accumulators of
-//                      128 x 128 int32 (all 512 TMEM columns), warps 2-9 drain TMEM (tcgen05.ld)
-//                      into FP64 registers (64 columns per thread) and add the tile into C with a
-//                      single read-modify-write that overlaps the next tile's MMAs. Only 4 groups fit in TMEM, so a
-//                      tile runs two passes over K: groups 4..6 (all 7 slices), then 0..3
-//                      (slices 0..3). K is cut in chunks short enough that no int32 accumulator
-//                      can overflow (7 pairs x 128^2 x K_chunk < 2^31).
+//   oz_rowexp_kernel     E[b][i] + range guard    (one pass over A, row max and sum of squares)
+//   oz_gram_prep_*       the same for A = X_b^T, fused with C_b = X_b^T Y_b (one pass over X)
+//   oz_slice_kernel      digits, K-major int8 slices [b][p][i][kpad]
+//   oz_syrk_pair_kernel  persistent, warp-specialised, 2-CTA clusters (tcgen05 cta_group::2,
+//                        M = 256, N = 128, K = 32): warp 0 of each CTA issues the TMA loads
+//                        (SWIZZLE_32B boxes, its own 128 rows of A_I and 64 rows of A_J), warp 1
+//                        of the leader issues the MMAs into 4 weight-group accumulators of
+//                        128 x 128 int32 (all 512 TMEM columns), warps 2-9 of both CTAs drain TMEM
+//                        (tcgen05.ld) into FP64 registers and add the tile into C with a single
+//                        read-modify-write that overlaps the next tile's MMAs. Only 4 groups fit in
+//                        TMEM, so a tile runs two passes over K: groups 4..6 (all 7 slices), then
+//                        0..3 (slices 0..3). K is cut in chunks short enough that no int32
+//                        accumulator can overflow (7 pairs x 128^2 x K_chunk < 2^31).
+//   oz_dotb_pair_kernel  the Gram-form hold-out w^T T w on the same machinery.
+// Every product has a device-side range guard (OZ_RANGE_BITS below) with a gated FP64 DMMA fallback.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -36,11 +39,9 @@
 namespace rp {
 
 constexpr int OZ_S = 7;  // slices: balanced base-256 digits of a 54-bit fixed-point value
-constexpr int OZ_BM = 128, OZ_BK = 32, OZ_STAGES = 3, OZ_GP = 4;
+constexpr int OZ_BM = 128, OZ_BK = 32, OZ_GP = 4;
 constexpr int OZ_SYRK_THREADS = 320;  // producer, MMA, 8 epilogue warps (SYRK and hold-out kernels)
 constexpr int OZ_SLICE = OZ_BM * OZ_BK;             // bytes of one 128 x 32 slice tile
-constexpr int OZ_STAGE = 2 * OZ_S * OZ_SLICE;        // A_I and A_J, all slices
-constexpr size_t OZ_SMEM = 1024 + (size_t)OZ_STAGES * OZ_STAGE + 128 + 4 * 128 * 8;  // + hold-out row reduction
 // Row exponent marking a row with a NaN or infinity: the entries it touches are NaN, as in FP64.
 constexpr int OZ_NONFINITE = 0x7fffffff;
 
@@ -63,39 +64,68 @@ struct OzIn {  // A_b: M x K column-major, element (i, k) at A + b * bstride + k
 
 // ------------------------------------------------------------------ preprocessing
 
+// Range guard. Per-row scaling truncates every entry of row i at 2^(E_i - 54), E_i the exponent of
+// the row's largest entry: normwise (relative to sqrt(C_ii C_jj)) this is always FP64-level, but an
+// entry 2^g below the row max keeps only 54 - g bits, so when the BULK of a row sits far below its
+// largest entry (a huge outlier among unit-scale values, heavy tails) the small entries of C --
+// and the small-eigenvalue directions a later Cholesky solve depends on -- lose accuracy that
+// FP64 keeps. The guard measures that gap as the row's largest exponent minus the mean exponent of
+// its nonzero entries (a geometric mean: Gaussian rows ~2.5 bits, sparse rows count only their
+// nonzeros) and sets *guard when it exceeds the product's bit budget (OZ_RANGE_BITS for the Gram
+// blocks and the Cholesky trailing updates; the hold-out's quadratic form only needs normwise
+// accuracy and uses OZ_RANGE_BITS_DOT). Every tensor-core kernel of the call then exits at once and
+// the gated FP64 DMMA kernel launched beside it computes the product. Zero and non-finite rows are
+// not guarded (zeros are exact; NaN/inf propagate).
+constexpr int OZ_RANGE_BITS = 10;
+constexpr int OZ_RANGE_BITS_DOT = 24;
+RP_DEVINL int oz_biased_exp(double v) { return (int)((__double_as_longlong(v) >> 52) & 0x7ff); }
+RP_DEVINL bool oz_out_of_range(double mx, double se, double nz, int bits) {
+  return nz > 0.0 && mx > 0.0 && mx <= 1.79769313486231570e308 && (double)oz_biased_exp(mx) - se / nz > (double)bits;
+}
+
 // E[b][i]: exponent with max_k |a_ik| < 2^E (0 for an all-zero row, OZ_NONFINITE if any entry is
-// NaN or infinite).
+// NaN or infinite), and the range guard (range_bits).
 // One CTA per 32 rows: 8 warps stride over k (each warp reads 32 contiguous rows of A per k:
-// coalesced), then a max-reduction over the warps in shared memory.
-__global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E) {
-  __shared__ double smx[8][32];
+// coalesced), then a max / sum-of-squares reduction over the warps in shared memory.
+__global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E, int* guard, int range_bits) {
+  __shared__ double smx[8][32], sse[8][32], snz[8][32];
   __shared__ int sfin[8][32];
   const int b = blockIdx.y, lane = threadIdx.x & 31, wk = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + lane;
   const int mp = in.mpad();
-  double mx = 0.0;
+  double mx = 0.0, se = 0.0, nz = 0.0;
   bool finite = true;
+  const int64_t kend = in.tri ? (i + 1 < in.K ? i + 1 : in.K) : in.K;  // T: columns k <= i
   if (i < in.M) {
     const double* x = in.A + (int64_t)b * in.bstride + i;
-    const int64_t kend = in.tri ? (i + 1 < in.K ? i + 1 : in.K) : in.K;  // T: columns k <= i
 #pragma unroll 4
     for (int64_t k = wk; k < kend; k += 8) {
-      const double v = fabs(__ldcs(x + k * in.lda));
+      double v = fabs(__ldcs(x + k * in.lda));
       finite &= (v <= 1.79769313486231570e308);  // false for NaN and inf
+      if (in.tri && k == i) v *= 0.5;             // T's diagonal
       mx = fmax(mx, v);
+      if (v != 0.0) {
+        se += (double)oz_biased_exp(v);
+        nz += 1.0;
+      }
     }
   }
   smx[wk][lane] = mx;
+  sse[wk][lane] = se;
+  snz[wk][lane] = nz;
   sfin[wk][lane] = finite ? 1 : 0;
   __syncthreads();
   if (E != nullptr && wk == 0 && i < mp) {
     for (int w = 1; w < 8; ++w) {
       mx = fmax(mx, smx[w][lane]);
+      se += sse[w][lane];
+      nz += snz[w][lane];
       finite = finite && sfin[w][lane];
     }
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);
     E[(int64_t)b * mp + i] = (i < in.M && !finite) ? OZ_NONFINITE : e;
+    if (guard != nullptr && i < in.M && finite && oz_out_of_range(mx, se, nz, range_bits)) atomicOr(guard, 1);
   }
 }
 
@@ -118,15 +148,16 @@ RP_DEVINL int oz_exp_code(double mx) {  // mx = +inf marks a NaN/inf entry
 template <int MT>
 __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int64_t ldx, int64_t rows, int d,
                                                            const double* Y, int64_t ldy, int m, int nchunk,
-                                                           double* Cp, double* Mp, int mp, int* E, double* C) {
+                                                           double* Cp, double* Mp, int mp, int* E, double* C,
+    int* guard) {
   constexpr int MM = MT > 0 ? MT : 1;
   const int b = blockIdx.z, ch = blockIdx.y;
   const int i0 = blockIdx.x * 1024 + threadIdx.x;
   const int64_t r0 = rows * ch / nchunk, r1 = rows * (ch + 1) / nchunk;
-  double acc[4][MM], mx[4];
+  double acc[4][MM], mx[4], se[4], nz[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    mx[j] = 0.0;
+    mx[j] = se[j] = nz[j] = 0.0;
 #pragma unroll
     for (int o = 0; o < MM; ++o) acc[j][o] = 0.0;
   }
@@ -143,6 +174,10 @@ __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int6
         const double xv = __ldcs(x + r * ldx + 256 * j);
         const double av = fabs(xv);
         mx[j] = (av <= 1.79769313486231570e308) ? fmax(mx[j], av) : __longlong_as_double(0x7ff0000000000000LL);
+        if (av != 0.0) {
+          se[j] += (double)oz_biased_exp(av);
+          nz[j] += 1.0;
+        }
 #pragma unroll
         for (int o = 0; o < MM; ++o) acc[j][o] = fma(xv, yv[o], acc[j][o]);
       }
@@ -154,6 +189,7 @@ __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int6
     // compile-time bound on o (a runtime bound would index acc dynamically: local memory)
     if (nchunk == 1) {
       if (E != nullptr && i < mp) E[(int64_t)b * mp + i] = i < d ? oz_exp_code(mx[j]) : 0;
+      if (guard != nullptr && i < d && oz_out_of_range(mx[j], se[j], nz[j], OZ_RANGE_BITS)) atomicOr(guard, 1);
       if (i < d) {
 #pragma unroll
         for (int o = 0; o < MM; ++o)
@@ -161,6 +197,8 @@ __global__ void __launch_bounds__(256) oz_gram_prep_kernel(const double* X, int6
       }
     } else if (i < d) {
       Mp[((int64_t)b * nchunk + ch) * d + i] = mx[j];
+      Mp[((int64_t)(gridDim.z + b) * nchunk + ch) * d + i] = se[j];  // exponent sums and nonzero counts
+      Mp[((int64_t)(2 * gridDim.z + b) * nchunk + ch) * d + i] = nz[j];  // after the maxima
 #pragma unroll
       for (int o = 0; o < MM; ++o)
         if (o < m) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
@@ -179,7 +217,8 @@ constexpr size_t OZ_GP_SMEM = sizeof(double) * OZ_GP_STAGES * OZ_GP_ROW + 2 * OZ
 template <int MT>
 __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X, int64_t ldx, int64_t rows, int d,
                                                                 const double* Y, int64_t ldy, int m, int nchunk,
-                                                                double* Cp, double* Mp, int mp, int* E, double* C) {
+                                                                double* Cp, double* Mp, int mp, int* E, double* C,
+    int* guard) {
   constexpr int MM = MT > 0 ? MT : 1;
   extern __shared__ __align__(16) double gp_smem[];
   double* sx = gp_smem;  // [stage][OZ_GP_ROW]
@@ -209,10 +248,10 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
     }
   };
   for (int s2 = 0; s2 < OZ_GP_STAGES - 1; ++s2) issue(s2);
-  double acc[4][MM], mx[4];
+  double acc[4][MM], mx[4], se[4], nz[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    mx[j] = 0.0;
+    mx[j] = se[j] = nz[j] = 0.0;
 #pragma unroll
     for (int o = 0; o < MM; ++o) acc[j][o] = 0.0;
   }
@@ -230,6 +269,10 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
         const double xv = xr[tid + 256 * j];
         const double av = fabs(xv);
         mx[j] = (av <= 1.79769313486231570e308) ? fmax(mx[j], av) : __longlong_as_double(0x7ff0000000000000LL);
+        if (av != 0.0) {
+          se[j] += (double)oz_biased_exp(av);
+          nz[j] += 1.0;
+        }
 #pragma unroll
         for (int o = 0; o < MM; ++o) acc[j][o] = fma(xv, yv[o], acc[j][o]);
       }
@@ -242,6 +285,7 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
     const int i = i0 + 256 * j;
     if (nchunk == 1) {
       if (E != nullptr && i < mp) E[(int64_t)b * mp + i] = i < d ? oz_exp_code(mx[j]) : 0;
+      if (guard != nullptr && i < d && oz_out_of_range(mx[j], se[j], nz[j], OZ_RANGE_BITS)) atomicOr(guard, 1);
       if (i < d) {
 #pragma unroll
         for (int o = 0; o < MM; ++o)
@@ -249,6 +293,8 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
       }
     } else if (i < d) {
       Mp[((int64_t)b * nchunk + ch) * d + i] = mx[j];
+      Mp[((int64_t)(gridDim.z + b) * nchunk + ch) * d + i] = se[j];  // exponent sums and nonzero counts
+      Mp[((int64_t)(2 * gridDim.z + b) * nchunk + ch) * d + i] = nz[j];  // after the maxima
 #pragma unroll
       for (int o = 0; o < MM; ++o)
         if (o < m) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
@@ -257,7 +303,7 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
 }
 
 __global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, int d, int m, int nchunk, int mp,
-                                           int* E, double* C) {
+                                           int* E, double* C, int nblocks, int* guard) {
   const int b = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= mp) return;
@@ -267,8 +313,14 @@ __global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, i
   }
   if (E != nullptr) {
     double mx = 0.0;
-    for (int c = 0; c < nchunk; ++c) mx = fmax(mx, Mp[((int64_t)b * nchunk + c) * d + i]);
+    double se = 0.0, nz = 0.0;
+    for (int c = 0; c < nchunk; ++c) {
+      mx = fmax(mx, Mp[((int64_t)b * nchunk + c) * d + i]);
+      se += Mp[((int64_t)(nblocks + b) * nchunk + c) * d + i];
+      nz += Mp[((int64_t)(2 * nblocks + b) * nchunk + c) * d + i];
+    }
     E[(int64_t)b * mp + i] = oz_exp_code(mx);
+    if (guard != nullptr && oz_out_of_range(mx, se, nz, OZ_RANGE_BITS)) atomicOr(guard, 1);
   }
   for (int o = 0; o < m; ++o) {
     double s = 0.0;
@@ -284,7 +336,9 @@ __global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, i
 // load latency otherwise).
 constexpr int OZ_SLICE_IW = 128;
 constexpr size_t OZ_SLICE_SMEM = sizeof(uint32_t) * OZ_S * OZ_SLICE_IW * 17;
-__global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, int8_t* slices, int64_t kpad) {
+__global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, int8_t* slices, int64_t kpad,
+                                                       const int* guard) {
+  if (guard != nullptr && *guard) return;  // out of range: the FP64 fallback runs instead
   constexpr int IW = OZ_SLICE_IW;
   extern __shared__ uint32_t oz_dig_raw[];  // dig[p][i][k/4], 4 digits per word, padded rows
   uint32_t(*dig)[IW][17] = reinterpret_cast<uint32_t(*)[IW][17]>(oz_dig_raw);
@@ -361,13 +415,14 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
   }
 }
 
-inline cudaError_t oz_slice_launch(const OzIn& in, const int* E, int8_t* slices, int64_t kpad, cudaStream_t st) {
+inline cudaError_t oz_slice_launch(const OzIn& in, const int* E, int8_t* slices, int64_t kpad, const int* guard,
+                                   cudaStream_t st) {
   static const cudaError_t attr =
       cudaFuncSetAttribute(oz_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SLICE_SMEM);
   if (attr != cudaSuccess) return attr;
   const int mp = in.mpad();
   oz_slice_kernel<<<dim3((unsigned)((kpad + 255) / 256), (mp + OZ_SLICE_IW - 1) / OZ_SLICE_IW, in.nbatch), 256,
-                    OZ_SLICE_SMEM, st>>>(in, E, slices, kpad);
+                    OZ_SLICE_SMEM, st>>>(in, E, slices, kpad, guard);
   return cudaSuccess;  // launch errors are picked up by the caller's RP_LAUNCH_CHECK
 }
 
@@ -383,19 +438,6 @@ RP_DEVINL uint64_t oz_desc_sw32(uint32_t saddr) {
 // kind::i8 instruction descriptor: s32 accumulate, signed A and B, both K-major, M = N = 128
 constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(128 >> 3) << 17) |
                               ((uint32_t)(OZ_BM >> 4) << 24);
-
-RP_DEVINL void oz_mma(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(dtmem),
-      "l"(adesc), "l"(bdesc), "r"(OZ_IDESC), "r"(accumulate));
-}
-
-RP_DEVINL void oz_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
 
 // All products S_p S_q^T of one K-step whose weight group g = p + q lies in [G0, G0 + OZ_GP), into
 // accumulator slab g - G0. G0 is a compile-time constant so the (p, q) list is fully unrolled
@@ -430,22 +472,6 @@ RP_DEVINL void oz_issue_kstep(uint32_t tmem, uint64_t da0, uint64_t db0, uint32_
 }
 
 // Whole-warp variants (the MMA issuer warp runs its loop converged; one elected lane commits).
-RP_DEVINL void oz_commit_warp(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
-      : "memory");
-}
-
-RP_DEVINL void oz_commit_mc_warp(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
 RP_DEVINL void oz_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 RP_DEVINL void oz_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
@@ -505,230 +531,16 @@ RP_DEVINL void oz_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// Lower 128 x 128 tiles (I, J <= I) of one matrix: I(I+1)/2 before row I.
-RP_DEVINL void oz_tile(int lin, int per, int& b, int& I, int& J) {
-  b = lin / per;
-  const int t = lin - b * per;
-  int i = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while ((i + 1) * (i + 2) / 2 <= t) ++i;
-  while (i * (i + 1) / 2 > t) --i;
-  I = i;
-  J = t - i * (i + 1) / 2;
-}
-
-// Pairs of lower tiles (I, 2jp), (I, 2jp + 1) with 2jp <= I: floor(I/2) + 1 pairs in row I.
-RP_DEVINL void oz_pair(int lin, int per, int& b, int& I, int& jp) {
-  b = lin / per;
-  int t = lin - b * per, i = 0;
-  while (t >= (i >> 1) + 1) {
-    t -= (i >> 1) + 1;
-    ++i;
-  }
-  I = i;
-  jp = t;
-}
-
 struct OzArgs {
   const int* E;      // [nbatch][Mp]
   double* C;         // C_b at C + b * cstride, column-major, leading dimension ldc
   int64_t ldc, cstride;
   int M, per, total_tiles;
   int Mp = 0;        // rows per (batch, slice) of the slice layout (pair kernel: M rounded up to 256)
-  int dbg = 0;       // experiments (RP_OZAKI_DBG, pair kernel): 1 = no operand loads, 2 = no MMAs
+  const int* guard = nullptr;  // range guard (oz_rowexp / gram prep): nonzero -> the FP64 fallback runs instead
   int subtract;      // 0: C = A A^T, 1: C -= A A^T
   int64_t kpad, kchunk;
 };
-
-// CL = 2: a cluster of two CTAs computes tiles (I, 2jp) and (I, 2jp + 1), which share the
-// A_I operand: each CTA loads half of the A_I slices and multicasts them to both, and the
-// stage is released to the producers by both CTAs' MMAs (commit multicast), halving the A
-// traffic from L2. The upper tile of a pair on the diagonal (J = I + 1) is computed but not
-// stored.
-template <int CL>
-__global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
-    oz_syrk_kernel(const __grid_constant__ CUtensorMap tm, OzArgs a) {
-  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
-  uint64_t* empty = full + OZ_STAGES;
-  uint64_t* tfull = empty + OZ_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nchunks = (int)((a.kpad + a.kchunk - 1) / a.kchunk);
-
-  const int rank = CL == 2 ? (int)oz_cluster_rank() : 0;
-  const int unit0 = CL == 2 ? blockIdx.x / 2 : blockIdx.x, ustep = CL == 2 ? gridDim.x / 2 : gridDim.x;
-  const int mt = a.M / OZ_BM;
-  // work unit -> (b, I, J) of this CTA; valid = a lower tile inside the matrix
-  auto unit_tile = [&](int u, int& b, int& I, int& J) {
-    if (CL == 2) {
-      int jp;
-      oz_pair(u, a.per, b, I, jp);
-      J = 2 * jp + rank;
-    } else {
-      oz_tile(u, a.per, b, I, J);
-    }
-    return J <= I;
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);  // CL == 2: released by both CTAs' MMAs
-    }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  oz_fence_before();
-  __syncthreads();
-  if (CL == 2) oz_cluster_sync();  // the peer's barriers exist before any multicast
-  oz_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      int it = 0;
-      for (int u = unit0; u < a.total_tiles; u += ustep) {
-        int b, I, J;
-        unit_tile(u, b, I, J);
-        const int Jl = J < mt ? J : I;  // past the last column tile: load a valid (unused) tile
-        const int rowA = b * OZ_S * a.Mp + I * OZ_BM, rowB = b * OZ_S * a.Mp + Jl * OZ_BM;
-        for (int pass = 1; pass >= 0; --pass) {
-          const int ns = pass ? OZ_S : OZ_GP;  // slices the pass reads
-          const int half = (ns + 1) / 2;
-          const int pa0 = CL == 2 ? rank * half : 0, pa1 = CL == 2 ? (rank ? ns : half) : ns;
-          for (int64_t k = 0; k < a.kpad; k += OZ_BK, ++it) {
-            const int st = it % OZ_STAGES;
-            mbar_wait(&empty[st], ((it / OZ_STAGES) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * OZ_SLICE));
-            uint8_t* sa = smem + st * OZ_STAGE;
-            uint8_t* sb = sa + OZ_S * OZ_SLICE;
-            for (int p = pa0; p < pa1; ++p) {
-              if (CL == 2)
-                oz_tma_2d_mc(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.Mp, &full[st], (uint16_t)3);
-              else
-                oz_tma_2d(sa + p * OZ_SLICE, &tm, (int)k, rowA + p * a.Mp, &full[st]);
-            }
-            for (int p = 0; p < ns; ++p) oz_tma_2d(sb + p * OZ_SLICE, &tm, (int)k, rowB + p * a.Mp, &full[st]);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (the whole warp runs the loop, one elected lane issues) ----------------
-    {
-      int it = 0, item = 0;
-      for (int u = unit0; u < a.total_tiles; u += ustep) {
-        for (int pass = 1; pass >= 0; --pass) {
-          const int g0 = pass * OZ_GP;
-          for (int ch = 0; ch < nchunks; ++ch, ++item) {
-            mbar_wait(tempty, (item & 1) ^ 1);  // the epilogue has drained the accumulators
-            oz_fence_after();
-            const int64_t kb = ch * a.kchunk, ke = (kb + a.kchunk < a.kpad) ? kb + a.kchunk : a.kpad;
-            for (int64_t k = kb; k < ke; k += OZ_BK, ++it) {
-              const int st = it % OZ_STAGES;
-              mbar_wait(&full[st], (it / OZ_STAGES) & 1);
-              oz_fence_after();
-              const uint32_t sa = smem_u32(smem + st * OZ_STAGE);
-              const uint32_t sb = sa + OZ_S * OZ_SLICE;
-              const bool first = (k == kb);
-              if (g0)
-                oz_issue_kstep<OZ_GP, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
-              else
-                oz_issue_kstep<0, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
-              // frees the stage (in both CTAs of a pair) once these MMAs have read it
-              if (CL == 2)
-                oz_commit_mc_warp(&empty[st], (uint16_t)3);
-              else
-                oz_commit_warp(&empty[st]);
-            }
-            oz_commit_warp(tfull);
-          }
-        }
-      }
-    }
-  } else {
-    // ---------------- epilogue (warps 2..9: TMEM lane quarter = warp % 4, column half) ----------------
-    // Both passes of a tile are drained from TMEM into FP64 registers (64 columns per thread) and
-    // the accumulators released right away, so the MMAs of the next pass / tile start at once; the
-    // tile is then added into C with a single read-modify-write that overlaps those MMAs.
-    const int quarter = warp & 3;
-    const int chalf = (warp - 2) >> 2;
-    const int row_in_tile = quarter * 32 + lane;
-    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
-    int item = 0;
-    for (int u = unit0; u < a.total_tiles; u += ustep) {
-      int b, I, J;
-      const bool valid = unit_tile(u, b, I, J);
-      const int i = I * OZ_BM + row_in_tile;
-      const int* Eb = a.E + (int64_t)b * a.Mp;
-      const int ei = Eb[i];
-      double acc[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
-      for (int pass = 1; pass >= 0; --pass) {
-        const int g0 = pass * OZ_GP;
-        for (int ch = 0; ch < nchunks; ++ch, ++item) {
-          mbar_wait(tfull, item & 1);
-          oz_fence_after();
-#pragma unroll
-          for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
-            if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
-            const double w = ldexp(1.0, -8 * (g0 + g) - 12);
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint32_t v[16];
-              oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), v);
-#pragma unroll
-              for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)v[c], w, acc[q4 * 16 + c]);
-            }
-          }
-          oz_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(tempty);
-        }
-      }
-      if (!valid) continue;  // the upper tile of a diagonal pair: accumulators drained only
-#ifdef OZ_DBG_NOSTORE
-      if (acc[0] != 12345.0) continue;  // experiments: TMEM drain without the C read-modify-write
-#endif
-      double* dst0 = a.C + (int64_t)b * a.cstride + (int64_t)(J * OZ_BM + chalf * 64) * a.ldc + i;
-      const int* Ej = Eb + J * OZ_BM + chalf * 64;
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        // every load of a 16-column group is issued before its stores
-        double old[16];
-        if (a.subtract) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) old[c] = __ldcg(dst0 + (int64_t)(q4 * 16 + c) * a.ldc);
-        }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const int ej = Ej[q4 * 16 + c];
-          double v;
-          if (ei == OZ_NONFINITE || ej == OZ_NONFINITE) {
-            v = __longlong_as_double(0x7ff8000000000000LL);
-          } else {
-            v = ldexp(acc[q4 * 16 + c], ei + ej);
-            if (a.subtract) v = old[c] - v;
-          }
-          dst0[(int64_t)(q4 * 16 + c) * a.ldc] = v;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (CL == 2) oz_cluster_sync();  // no CTA leaves while its peer may still signal it
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
-}
 
 // ------------------------------------------------------------------ CTA-pair (cta_group::2) SYRK
 // A 2-CTA cluster computes a 256 x 128 block (sub-tile rows 2 I2 and 2 I2 + 1, column tile J) with
@@ -826,6 +638,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
   const int nchunks = (int)((a.kpad + a.kchunk - 1) / a.kchunk);
   const int unit0 = blockIdx.x / 2, ustep = gridDim.x / 2;
   const int mt = a.M / OZ_BM;  // sub-tile rows that exist (rows of the padded pair past mt are zero)
+  if (a.guard != nullptr && *a.guard) return;  // out of range: both CTAs leave before any cluster barrier
 
   if (tid == 0) {
     for (int s = 0; s < OZ_PSTAGES; ++s) {
@@ -862,10 +675,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
           for (int64_t k = 0; k < a.kpad; k += OZ_BK, ++it) {
             const int st = it % OZ_PSTAGES;
             oz_mbar_wait_cluster(&empty[st], ((it / OZ_PSTAGES) & 1) ^ 1);
-            if (a.dbg & 1) {
-              if (rank == 0) mbar_arrive(&full[st]);
-              continue;
-            }
             if (rank == 0) mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * (OZ_SLICE + OZ_PSLICE_B)));
             uint8_t* sa = smem + st * OZ_PSTAGE;
             uint8_t* sb = sa + OZ_S * OZ_SLICE;
@@ -896,8 +705,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
               const uint32_t sa = smem_u32(smem + st * OZ_PSTAGE);
               const uint32_t sb = sa + OZ_S * OZ_SLICE;
               const bool first = (k == kb);
-              if (a.dbg & 2) {
-              } else if (g0) {
+              if (g0) {
                 oz_issue_kstep<OZ_GP, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
               } else {
                 oz_issue_kstep<0, OZ_PSLICE_B, true>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), first);
@@ -1015,9 +823,14 @@ inline size_t oz_eb(int M, int nbatch) { return ((size_t)nbatch * M * sizeof(int
 // Rows of the SYRK slice layout: M rounded up to the 256-row blocks of the CTA-pair kernel.
 inline int oz_mp(int M) { return (M + 255) / 256 * 256; }
 
+// Workspace of one tensor-core product: a 1 KB header (the range guard int), the row exponents
+// E[b][mp], then the K-major slices.
+constexpr size_t OZ_HDR = 1024;
+inline int* oz_guard_of(void* work) { return reinterpret_cast<int*>(work); }
+
 inline size_t oz_workspace_bytes(int M, int64_t K, int nbatch) {
   const int mp = oz_mp(M);
-  return oz_eb(mp, nbatch) + (size_t)nbatch * OZ_S * mp * (size_t)oz_kpad(K);
+  return OZ_HDR + oz_eb(mp, nbatch) + (size_t)nbatch * OZ_S * mp * (size_t)oz_kpad(K);
 }
 
 // Shapes the tensor-core path takes: 128-row tiles, int32 TMA coordinates.
@@ -1026,51 +839,49 @@ inline bool oz_supported(int M, int64_t K, int nbatch) {
          oz_encode_fn() != nullptr;
 }
 
-// Exponents + K-major slices of a batch of column-major matrices (rows padded to in.mpad()).
-inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, cudaStream_t st) {
+// Exponents (+ range guard with the given bit budget) and K-major slices of a batch of column-major matrices (rows padded
+// to in.mpad()). The guard must have been cleared by the caller.
+inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, int* guard, int range_bits,
+                      cudaStream_t st) {
   const int mp = in.mpad();
-  oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E);
+  oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E, guard, range_bits);
   RP_LAUNCH_CHECK("ozaki rowexp");
-  cudaError_t e = oz_slice_launch(in, E, slices, kpad, st);
+  cudaError_t e = oz_slice_launch(in, E, slices, kpad, guard, st);
   if (e != cudaSuccess) return cuda_status(e, "ozaki slice attributes");
   RP_LAUNCH_CHECK("ozaki slice");
   return RP_OK;
 }
 
-// RP_OZAKI_PAIR=0: independent CTAs (128 x 128 tiles) instead of CTA pairs (256 x 128 blocks)
-inline bool oz_pair_enabled() {
-  static const bool pair = [] {
-    const char* e = getenv("RP_OZAKI_PAIR");
-    return !(e && e[0] == '0');
-  }();
-  return pair;
-}
-
-// C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b.
-// exps_ready: the row exponents are already in the workspace (E[b * oz_mp(M) + i], e.g. from
-// oz_gram_prep_kernel), so only the slicing pass runs.
+// C_b (lower 128 x 128 tiles, each complete) = / -= A_b A_b^T for nbatch column-major M x K A_b,
+// on 2-CTA clusters. exps_ready: the row exponents and the range guard are already in the
+// workspace (oz_gram_prep_kernel), so only the slicing pass runs; otherwise the guard is cleared
+// and set here. When the guard is set every kernel of this call exits at once: the caller
+// launches the gated FP64 fallback (GemmArgs::run_if_set = oz_guard_of(work)) behind it.
 inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool subtract, void* work,
                    cudaStream_t st, const char* prof_name = "oz_syrk", bool exps_ready = false) {
-  const bool pair = oz_pair_enabled();
   OzIn pin = in;
-  pin.Mpad = pair ? oz_mp(in.M) : in.M;
+  pin.Mpad = oz_mp(in.M);
   const int mp = pin.Mpad;
-  int* E = reinterpret_cast<int*>(work);
-  int8_t* slices = reinterpret_cast<int8_t*>(work) + oz_eb(mp, in.nbatch);
+  int* guard = oz_guard_of(work);
+  int* E = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(work) + OZ_HDR);
+  int8_t* slices = reinterpret_cast<int8_t*>(work) + OZ_HDR + oz_eb(mp, in.nbatch);
   const int64_t kpad = oz_kpad(in.K);
   {
     ProfScope prof("oz_prep", st);
-    if (exps_ready && pair) {
-      cudaError_t e = oz_slice_launch(pin, E, slices, kpad, st);
+    if (exps_ready) {
+      cudaError_t e = oz_slice_launch(pin, E, slices, kpad, guard, st);
       if (e != cudaSuccess) return cuda_status(e, "ozaki slice attributes");
       RP_LAUNCH_CHECK("ozaki slice");
     } else {
-      int rc = oz_prepare(pin, E, slices, kpad, st);
+      cudaError_t e = cudaMemsetAsync(guard, 0, sizeof(int), st);
+      if (e != cudaSuccess) return cuda_status(e, "ozaki guard");
+      int rc = oz_prepare(pin, E, slices, kpad, guard, OZ_RANGE_BITS, st);
       if (rc) return rc;
     }
   }
-  CUtensorMap tm;
-  if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * mp))
+  CUtensorMap tm, tmB;
+  if (!oz_tensor_map(&tm, slices, kpad, (int64_t)in.nbatch * OZ_S * mp) ||
+      !oz_tensor_map(&tmB, slices, kpad, (int64_t)in.nbatch * OZ_S * mp, 64))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
   OzArgs a;
   a.E = E;
@@ -1079,6 +890,7 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   a.cstride = cstride;
   a.M = in.M;
   a.Mp = mp;
+  a.guard = guard;
   const int mt = in.M / OZ_BM;
   a.subtract = subtract ? 1 : 0;
   a.kpad = kpad;
@@ -1086,74 +898,17 @@ inline int oz_syrk(const OzIn& in, double* C, int64_t ldc, int64_t cstride, bool
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (pair) {
-    CUtensorMap tmB;
-    if (!oz_tensor_map(&tmB, slices, kpad, (int64_t)in.nbatch * OZ_S * mp, 64))
-      return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
-    a.per = 0;
-    for (int i2 = 0; i2 < (mt + 1) / 2; ++i2) a.per += (2 * i2 + 2 < mt ? 2 * i2 + 2 : mt);
-    a.total_tiles = a.per * in.nbatch;  // pair units
-    static const int dbg = [] {
-      const char* e = getenv("RP_OZAKI_DBG");
-      return e ? atoi(e) : 0;
-    }();
-    a.dbg = dbg;
-    cudaFuncSetAttribute(oz_syrk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM);
-    int pairs = sms / 2;
-    if (pairs > a.total_tiles) pairs = a.total_tiles;
-    {
-      ProfScope prof(prof_name, st);
-      oz_syrk_pair_kernel<<<2 * pairs, OZ_SYRK_THREADS, OZ_PSMEM, st>>>(tm, tmB, a);
-    }
-    RP_LAUNCH_CHECK("ozaki syrk (CTA pairs)");
-    return RP_OK;
-  }
-  // RP_OZAKI_CLUSTER=1 (with RP_OZAKI_PAIR=0): 2-CTA clusters sharing A_I by multicast. Measured
-  // slower at c4 (Gram kernel 21.3 vs 20.1 ms: the pair runs in lockstep and wastes the diagonal
-  // pair's upper tile).
-  static const bool cluster = [] {
-    const char* e = getenv("RP_OZAKI_CLUSTER");
-    return e && e[0] == '1';
-  }();
-  if (cluster && mt >= 2) {
-    // pairs of tiles sharing A_I on 2-CTA clusters (A multicast)
-    a.per = 0;
-    for (int i = 0; i < mt; ++i) a.per += i / 2 + 1;
-    a.total_tiles = a.per * in.nbatch;
-    auto k = oz_syrk_kernel<2>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(OZ_SYRK_THREADS);
-    cfg.dynamicSmemBytes = OZ_SMEM;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.gridDim = dim3(sms);
-    int clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess || clusters < 1) clusters = sms / 2;
-    (void)cudaGetLastError();
-    if (clusters > a.total_tiles) clusters = a.total_tiles;
-    cfg.gridDim = dim3(2 * clusters);
-    ProfScope prof(prof_name, st);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k, tm, a);
-    if (e != cudaSuccess) return cuda_status(e, "ozaki syrk (cluster)");
-    count_launch();
-    return RP_OK;
-  }
-  a.per = mt * (mt + 1) / 2;
-  a.total_tiles = a.per * in.nbatch;
-  const int grid = a.total_tiles < sms ? a.total_tiles : sms;
-  cudaFuncSetAttribute(oz_syrk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+  a.per = 0;
+  for (int i2 = 0; i2 < (mt + 1) / 2; ++i2) a.per += (2 * i2 + 2 < mt ? 2 * i2 + 2 : mt);
+  a.total_tiles = a.per * in.nbatch;  // pair units
+  cudaFuncSetAttribute(oz_syrk_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM);
+  int pairs = sms / 2;
+  if (pairs > a.total_tiles) pairs = a.total_tiles;
   {
     ProfScope prof(prof_name, st);
-    oz_syrk_kernel<1><<<grid, OZ_SYRK_THREADS, OZ_SMEM, st>>>(tm, a);
+    oz_syrk_pair_kernel<<<2 * pairs, OZ_SYRK_THREADS, OZ_PSMEM, st>>>(tm, tmB, a);
   }
-  RP_LAUNCH_CHECK("ozaki syrk");
+  RP_LAUNCH_CHECK("ozaki syrk (CTA pairs)");
   return RP_OK;
 }
 
@@ -1172,186 +927,12 @@ struct OzDotArgs {
   const double* W;
   int64_t ldw, w_stride;
   double* part;
+  const int* guard;  // range guard: nonzero -> exit (the FP64 fallback runs)
   int d, N, MpadA, MpadB, mtA, ntB, nbatch, a_shared, total_tiles;
   int64_t kpad;
 };
 
-__global__ void __launch_bounds__(OZ_SYRK_THREADS, 1)
-    oz_dotb_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzDotArgs a) {
-  extern __shared__ __align__(1024) uint8_t oz_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + OZ_STAGES * OZ_STAGE);
-  uint64_t* empty = full + OZ_STAGES;
-  uint64_t* tfull = empty + OZ_STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-  double* red = reinterpret_cast<double*>(smem + OZ_STAGES * OZ_STAGE + 128);  // [4][128]
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int per_I = a.nbatch * a.ntB;
-  auto decode = [&](int tile, int& b, int& I, int& J) {  // heaviest (largest I) first
-    const int rank = tile / per_I, rem = tile - rank * per_I;
-    I = a.mtA - 1 - rank;
-    b = rem / a.ntB;
-    J = rem - b * a.ntB;
-  };
-  auto ksteps = [&](int I) {
-    const int64_t ke = (int64_t)(I + 1) * OZ_BM < a.kpad ? (int64_t)(I + 1) * OZ_BM : a.kpad;
-    return (int)(ke / OZ_BK);
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < OZ_STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(tfull, 1);
-    mbar_init(tempty, 8);
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  oz_fence_before();
-  __syncthreads();
-  oz_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int it = 0;
-      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-        int b, I, J;
-        decode(tile, b, I, J);
-        const int ba = a.a_shared ? 0 : b;
-        const int rowA = ba * OZ_S * a.MpadA + I * OZ_BM, rowB = b * OZ_S * a.MpadB + J * OZ_BM;
-        const int nk = ksteps(I);
-        for (int pass = 1; pass >= 0; --pass) {
-          const int ns = pass ? OZ_S : OZ_GP;
-          for (int kk = 0; kk < nk; ++kk, ++it) {
-            const int st = it % OZ_STAGES;
-            mbar_wait(&empty[st], ((it / OZ_STAGES) & 1) ^ 1);
-            mbar_arrive_expect_tx(&full[st], (uint32_t)(2 * ns * OZ_SLICE));
-            uint8_t* sa = smem + st * OZ_STAGE;
-            uint8_t* sb = sa + OZ_S * OZ_SLICE;
-            for (int p = 0; p < ns; ++p) {
-              oz_tma_2d(sa + p * OZ_SLICE, &tmA, kk * OZ_BK, rowA + p * a.MpadA, &full[st]);
-              oz_tma_2d(sb + p * OZ_SLICE, &tmB, kk * OZ_BK, rowB + p * a.MpadB, &full[st]);
-            }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    {  // the whole warp runs the loop, one elected lane issues
-      int it = 0, item = 0;
-      for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-        int b, I, J;
-        decode(tile, b, I, J);
-        const int nk = ksteps(I);
-        for (int pass = 1; pass >= 0; --pass, ++item) {
-          const int g0 = pass * OZ_GP;
-          mbar_wait(tempty, (item & 1) ^ 1);
-          oz_fence_after();
-          for (int kk = 0; kk < nk; ++kk, ++it) {
-            const int st = it % OZ_STAGES;
-            mbar_wait(&full[st], (it / OZ_STAGES) & 1);
-            oz_fence_after();
-            const uint32_t sa = smem_u32(smem + st * OZ_STAGE);
-            const uint32_t sb = sa + OZ_S * OZ_SLICE;
-            if (g0)
-              oz_issue_kstep<OZ_GP, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
-            else
-              oz_issue_kstep<0, OZ_SLICE, false>(tmem, oz_desc_sw32(sa), oz_desc_sw32(sb), kk == 0);
-            oz_commit_warp(&empty[st]);
-          }
-          oz_commit_warp(tfull);
-        }
-      }
-    }
-  } else {
-    // epilogue warps 2..9: TMEM lane quarter = warp % 4, 64-column half = (warp - 2) / 4
-    const int quarter = warp & 3, chalf = (warp - 2) >> 2;
-    const int row_in_tile = quarter * 32 + lane;
-    const uint32_t tlane = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(chalf * 64);
-    int item = 0;
-    for (int tile = blockIdx.x; tile < a.total_tiles; tile += gridDim.x) {
-      int b, I, J;
-      decode(tile, b, I, J);
-      const int ba = a.a_shared ? 0 : b;
-      const int i = I * OZ_BM + row_in_tile;
-      const int ei = a.EA[(int64_t)ba * a.MpadA + i];
-      const int* EBb = a.EB + (int64_t)b * a.MpadB;
-      const double* Wrow = a.W + (int64_t)b * a.w_stride + (int64_t)i * a.ldw;
-      double acc[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) acc[c] = 0.0;
-      for (int pass = 1; pass >= 0; --pass, ++item) {
-        const int g0 = pass * OZ_GP;
-        mbar_wait(tfull, item & 1);
-        oz_fence_after();
-#pragma unroll
-        for (int g = OZ_GP - 1; g >= 0; --g) {  // smallest weights first
-          if (g0 + g >= OZ_S) continue;      // groups past S - 1 are not computed
-          const double w = ldexp(1.0, -8 * (g0 + g) - 12);
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            uint32_t t[16];
-            oz_ld16(tlane + (uint32_t)(g * 128 + q4 * 16), t);
-#pragma unroll
-            for (int c = 0; c < 16; ++c) acc[q4 * 16 + c] = fma((double)(int)t[c], w, acc[q4 * 16 + c]);
-          }
-        }
-        oz_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty);  // the next pass / tile may overwrite the accumulators
-      }
-      const int n0 = J * OZ_BM + chalf * 64;
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const int n = n0 + c;
-        double x = 0.0;
-        if (i < a.d && n < a.N) {
-          const int en = EBb[n];
-          x = (ei == OZ_NONFINITE || en == OZ_NONFINITE) ? __longlong_as_double(0x7ff8000000000000LL)
-                                                          : ldexp(acc[c], ei + en) * Wrow[n];
-        }
-        acc[c] = x;
-      }
-      // reduce-scatter over the warp's 32 rows, per 32 columns: lane L ends with column n0 + 32 hh + L
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-        for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-          const bool upper = (lane & s2) != 0;
-#pragma unroll
-          for (int j = 0; j < s2; ++j) {
-            const double send = upper ? acc[hh * 32 + j] : acc[hh * 32 + j + s2];
-            const double keep = upper ? acc[hh * 32 + j + s2] : acc[hh * 32 + j];
-            acc[hh * 32 + j] = keep + __shfl_xor_sync(0xffffffffu, send, s2);
-          }
-        }
-        red[quarter * 128 + chalf * 64 + hh * 32 + lane] = acc[hh * 32];
-      }
-      named_bar_sync(1, 256);
-      if (quarter == 0) {  // rows summed in quarter order
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int col = chalf * 64 + hh * 32 + lane;
-          const double tot = red[col] + red[128 + col] + red[256 + col] + red[384 + col];
-          const int n = J * OZ_BM + col;
-          if (n < a.N) a.part[((int64_t)b * a.mtA + I) * a.N + n] = tot;
-        }
-      }
-      named_bar_sync(1, 256);
-    }
-  }
-  __syncthreads();
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
-}
-
-// CTA-pair hold-out kernel: as oz_dotb_kernel, but a 2-CTA cluster computes sub-tile rows 2 I2
+// CTA-pair hold-out kernel: a 2-CTA cluster computes sub-tile rows 2 I2
 // and 2 I2 + 1 of T_b against the 128 columns J of W_b^T with tcgen05.mma.cta_group::2 (M = 256,
 // N = 128); each CTA stages its own 128 rows of T and 64 of the 128 W^T rows (the barrier
 // protocol of oz_syrk_pair_kernel). K runs to 128 (2 I2 + 2) for both rows of the pair (T is
@@ -1384,6 +965,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
     return (int)(ke / OZ_BK);
   };
   const int unit0 = blockIdx.x / 2, ustep = gridDim.x / 2;
+  if (a.guard != nullptr && *a.guard) return;  // out of range: both CTAs leave before any cluster barrier
 
   if (tid == 0) {
     for (int s = 0; s < OZ_PSTAGES; ++s) {
@@ -1545,11 +1127,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
 
 inline int64_t oz_rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-// Workspace of oz_holdout: exponents and slices of T (nA copies) and of W^T (nbatch).
+// Workspace of oz_holdout: guard header, exponents and slices of T (nA copies) and of W^T (nbatch).
 inline size_t oz_holdout_workspace(int d, int64_t N, int nbatch, bool a_shared) {
   const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = a_shared ? 1 : nbatch;
-  return (size_t)oz_rup((int64_t)na * mpa * 4, 1024) + (size_t)oz_rup((int64_t)nbatch * mpb * 4, 1024) +
+  return OZ_HDR + (size_t)oz_rup((int64_t)na * mpa * 4, 1024) + (size_t)oz_rup((int64_t)nbatch * mpb * 4, 1024) +
          (size_t)na * OZ_S * mpa * kpad + (size_t)nbatch * OZ_S * mpb * kpad;
 }
 
@@ -1559,14 +1141,16 @@ inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
          oz_encode_fn() != nullptr;
 }
 
-// part[b][I][n]: partials of w_n^T T_b w_n (sum over the ceil(d/128) entries).
+// part[b][I][n]: partials of w_n^T T_b w_n (sum over the ceil(d/128) entries). The range guard
+// covers both operands (rows of T and of W^T); when it trips the kernels exit and the caller's
+// gated FP64 fallback runs (as oz_syrk).
 inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
                       int64_t N, int nbatch, double* part, void* work, cudaStream_t st) {
   const bool shared = g_stride == 0;
-  const bool pair = oz_pair_enabled();
-  const int64_t mpa = oz_rup(d, pair ? 256 : OZ_BM), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
+  const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = shared ? 1 : nbatch;
-  uint8_t* w8 = reinterpret_cast<uint8_t*>(work);
+  int* guard = oz_guard_of(work);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(work) + OZ_HDR;
   int* EA = reinterpret_cast<int*>(w8);
   w8 += oz_rup((int64_t)na * mpa * 4, 1024);
   int* EB = reinterpret_cast<int*>(w8);
@@ -1578,13 +1162,15 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   ia.tri = 1;
   OzIn ib{W, ldw, w_stride, d, (int)N, nbatch};  // W_b^T: row n, column k at W + k*ldw + n
   ib.Mpad = (int)mpb;
-  int rc = oz_prepare(ia, EA, SA, kpad, st);
+  cudaError_t e = cudaMemsetAsync(guard, 0, sizeof(int), st);
+  if (e != cudaSuccess) return cuda_status(e, "ozaki guard");
+  int rc = oz_prepare(ia, EA, SA, kpad, guard, OZ_RANGE_BITS_DOT, st);
   if (rc) return rc;
-  rc = oz_prepare(ib, EB, SB, kpad, st);
+  rc = oz_prepare(ib, EB, SB, kpad, guard, OZ_RANGE_BITS_DOT, st);
   if (rc) return rc;
   CUtensorMap ta, tb;
   if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) ||
-      !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb, pair ? 64 : OZ_BM))
+      !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb, 64))
     return set_error(RP_ECUDA, "ozaki: cuTensorMapEncodeTiled failed");
   OzDotArgs a;
   a.EA = EA;
@@ -1593,6 +1179,7 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   a.ldw = ldw;
   a.w_stride = w_stride;
   a.part = part;
+  a.guard = guard;
   a.d = d;
   a.N = (int)N;
   a.MpadA = (int)mpa;
@@ -1601,22 +1188,17 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   a.ntB = (int)(mpb / OZ_BM);
   a.nbatch = nbatch;
   a.a_shared = shared ? 1 : 0;
-  a.total_tiles = (pair ? (a.mtA + 1) / 2 : a.mtA) * a.ntB * nbatch;
+  a.total_tiles = (a.mtA + 1) / 2 * a.ntB * nbatch;
   a.kpad = kpad;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (pair) {
-    int pairs = sms / 2;
-    if (pairs > a.total_tiles) pairs = a.total_tiles;
-    cudaFuncSetAttribute(oz_dotb_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM_DOT);
+  int pairs = sms / 2;
+  if (pairs > a.total_tiles) pairs = a.total_tiles;
+  cudaFuncSetAttribute(oz_dotb_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_PSMEM_DOT);
+  {
     ProfScope prof("oz_holdout", st);
     oz_dotb_pair_kernel<<<2 * pairs, OZ_SYRK_THREADS, OZ_PSMEM_DOT, st>>>(ta, tb, a);
-  } else {
-    const int grid = a.total_tiles < sms ? a.total_tiles : sms;
-    cudaFuncSetAttribute(oz_dotb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
-    ProfScope prof("oz_holdout", st);
-    oz_dotb_kernel<<<grid, OZ_SYRK_THREADS, OZ_SMEM, st>>>(ta, tb, a);
   }
   RP_LAUNCH_CHECK("ozaki holdout");
   return RP_OK;

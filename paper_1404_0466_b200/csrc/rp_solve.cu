@@ -8,6 +8,10 @@
 
 using namespace rp;
 
+namespace rp {
+int g_solve_lam = 0;  // rp_set_option("solve_lam", n): 0 = the planner's choice
+}
+
 static int launch_generic(int m, const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
   switch (m) {
     case 1: return launch_solve<0, 1, 0, 0>(a, grid, smem, st);
@@ -69,13 +73,11 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
       pl.fast = false;
     }
   }
-  static const int lam_env = [] {  // RP_SOLVE_LAM (experiments): force a specialised chunk size
-    const char* e = getenv("RP_SOLVE_LAM");
-    return e ? atoi(e) : 0;
-  }();
-  if (lam_env > 0 && q >= lam_env && has_solve_fast(m, pl.P, lam_env) &&
-      solve_smem_bytes(lam_env, m, pl.P) <= (size_t)maxsmem) {
-    pl.lam = lam_env;
+  // rp_set_option("solve_lam", n) (tests): force a specialised chunk size when it exists
+  const int lam_force = g_solve_lam;
+  if (lam_force > 0 && q >= lam_force && has_solve_fast(m, pl.P, lam_force) &&
+      ((m % 2 == 0) || ((q - lam_force) % 2 == 0)) && solve_smem_bytes(lam_force, m, pl.P) <= (size_t)maxsmem) {
+    pl.lam = lam_force;
     pl.fast = true;
   }
   if (pl.lam > 0) {
@@ -127,11 +129,6 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   a.chunks = pl.chunks;
   a.S = pl.S;
   a.Wc = (double*)work;
-  static const int dbg = [] {
-    const char* e = getenv("RP_SOLVE_DBG");
-    return e ? atoi(e) : 0;
-  }();
-  a.dbg = dbg;
   const int grid = nf * a.chunks;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
   if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");

@@ -61,8 +61,7 @@ struct SolveArgs {
   const double* tvals;
   int* flags;
   int q, m, d, nt, P, lam_per_cta, chunks, S;
-  int dbg;  // experiments only (RP_SOLVE_DBG): 1 = skip slab copies, 2 = skip diagonal solves
-  double* Wc;             // warp-specialised kernel: chunk-private W rows (dp x S per CTA)
+  double* Wc;             // chunk-private rows of the solution (dp x S per CTA)
   int64_t theta_bwd_off;  // offset of the transposed (backward) tile copy inside a fold's theta
 };
 
@@ -147,7 +146,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 
   for (int step = 0; step < a.nt; ++step) {
     const int I = BWD ? (a.nt - 1 - step) : step;
-    const int nslab = (a.dbg & 4) ? 0 : 4 * (BWD ? (a.nt - 1 - I) : I);  // dbg 4: diagonal steps only
+    const int nslab = 4 * (BWD ? (a.nt - 1 - I) : I);
     if (tid == 0) {  // warm L2 with this row's diagonal tile: its copy at the end of the row then hits
       const double* dt = theta + (int64_t)tile_index(I, I) * P * TILE_PLANE;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(dt), "r"((uint32_t)(P * TILE_PLANE * 8))
@@ -168,7 +167,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     // A stage is refilled once every warp has released its previous slab (empty[st]); only the
     // issuing thread waits for that, the other warps run ahead as far as the data allows.
     auto issue = [&](int s) {
-      if (tid == 0 && s < nslab && !(a.dbg & 1)) {
+      if (tid == 0 && s < nslab) {
         const int it = it0 + s, st = it % STG;
         if (it >= STG) mbar_wait(&empty[st], ((it / STG) + 1) & 1);
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
@@ -189,7 +188,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     for (int s = 0; s < nslab; ++s) {
       issue(s + 2);
       const int st = (it0 + s) % STG;
-      if (!(a.dbg & 1)) mbar_wait(&full[st], ((it0 + s) / STG) & 1);
+      mbar_wait(&full[st], ((it0 + s) / STG) & 1);
       const double* T = sT + st * stageT;
       const double* Wb = sW + st * stageW;
 #pragma unroll
@@ -322,7 +321,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       }
       __syncthreads();
       RP_SP_MARK(2);  // evaluate the 16 x 16 block
-      if (!(a.dbg & 2) && tid < cw) {
+      if (tid < cw) {
         const int l = tid / m;
         const double* Lv = sLev + l * 16 * 17;
         const double* ri = sRinv + l * 16;

@@ -210,14 +210,18 @@ class PicholEngine:
                 if self._folds_regular():
                     f0 = self.local_folds[0]
                     yyg = self.yy[:, c0:c1].contiguous() if len(self.groups) > 1 else self.yy
+                    off = int(self.row_off[f0])
                     call("rp_holdout_gram", ptr(self.G[f0]), d * d, ptr(self.C[f0, c0:]), self.m * d,
                          ptr(yyg[f0]), self.block_rows[f0], d, mg, ptr(W), ldw, W[0].numel(), q, self.nf,
+                         ptr(X[off:]), d, self.block_rows[0], ptr(Y[off:, c0:]), self.m,
                          ptr(out), ptr(self.ws_hold), st)
                 else:
                     yyg = self.yy[:, c0:c1].contiguous()
                     for i, f in enumerate(self.local_folds):
+                        off = int(self.row_off[f])
                         call("rp_holdout_gram", ptr(self.G[f]), d * d, ptr(self.C[f, c0:]), self.m * d,
                              ptr(yyg[f]), self.block_rows[f], d, mg, ptr(W[i]), ldw, W[0].numel(), q, 1,
+                             ptr(X[off:]), d, 0, ptr(Y[off:, c0:]), self.m,
                              ptr(out[i]), ptr(self.ws_hold), st)
             else:
                 if self._folds_regular():

@@ -117,8 +117,10 @@ class ExactEvaluator:
                 wsh = _dev.workspace(_lib.query("rp_holdout_workspace_size", n_val, d, 1, mg, nb))
                 if self.holdout == "gram":
                     yy_b = self.yy[f, c0:c1].expand(nb, mg).contiguous()
+                    off = int(self.row_off[f])
                     call("rp_holdout_gram", ptr(self.G[f]), 0, ptr(self.C[f, c0:]), 0, ptr(yy_b), n_val, d, mg,
-                         ptr(Wf), ldw, dp * ldw, 1, nb, ptr(res), ptr(wsh), st)
+                         ptr(Wf), ldw, dp * ldw, 1, nb, ptr(self.dX[off:]), d, 0, ptr(self.dY[off:, c0:]), m,
+                         ptr(res), ptr(wsh), st)
                 else:
                     off = int(self.row_off[f])
                     call("rp_holdout_direct", ptr(self.dX[off:]), d, 0, n_val, d, ptr(self.dY[off:, c0:]), m, mg,
