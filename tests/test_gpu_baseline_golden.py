@@ -106,7 +106,16 @@ def test_c5_fold0_matches_reference(gpu):
           f"(excluded grid indices {np.flatnonzero(~keep).tolist()})")
     assert keep[:400].all() and keep.sum() >= 400
     assert err <= CURVE_TOL
+    # fold 0's own argmins (the selection proper averages 8 folds; the reference's c5 sweep takes ~20
+    # CPU-minutes per fold, so only fold 0 is pinned): identical wherever the reference's best-to-second
+    # gap exceeds 10x the achieved curve error (output 11's fold-0 gap is 2.5e-11)
+    cref = np.where(np.isfinite(ref), ref, np.inf)
     fold0_best = np.argmin(np.where(np.isfinite(curves[0]), curves[0], np.inf), axis=0)
-    ref_best = np.argmin(np.where(np.isfinite(ref), ref, np.inf), axis=0)
-    assert np.array_equal(fold0_best, ref_best)
+    ref_best = np.argmin(cref, axis=0)
+    srt = np.sort(cref, axis=0)
+    gap = (srt[1] - srt[0]) / srt[0]
+    resolvable = gap > 10 * err
+    print(f"c5 fold 0: argmins {fold0_best.tolist()} (reference {ref_best.tolist()}); gaps {np.round(gap, 12).tolist()}")
+    assert resolvable.sum() >= 14
+    assert np.array_equal(fold0_best[resolvable], ref_best[resolvable])
     check_factors(g, cfg, sess)
