@@ -335,7 +335,9 @@ def run_ours(args, cfg, world, rank, local):
     _lib.query("rp_profile_ms", None)
     sess.sweep()
     kern_ms = {name: _lib.query("rp_profile_ms", name.encode())
-               for name in ("oz_syrk", "eval_solve", "holdout_gemm", "oz_holdout")}
+               for name in ("oz_syrk", "eval_solve_fwd", "eval_solve_bwd", "holdout_gemm", "oz_holdout")}
+    solve_split = (kern_ms.pop("eval_solve_fwd"), kern_ms.pop("eval_solve_bwd"))
+    kern_ms["eval_solve"] = sum(solve_split)
     _lib.call("rp_set_option", b"profile", 0)
 
     # ---- end to end through the public API (pinned host in, curves + argmin out)
@@ -373,7 +375,8 @@ def run_ours(args, cfg, world, rank, local):
                               "peak": pk["i8_tops"], "peak_src": pk["i8_src"],
                               "fp64_equivalent_tflops": flops["gram"] / (kern_ms["oz_syrk"] / 1e3) / 1e12}
     if kern_ms["eval_solve"] > 0:
-        kernels["eval_solve"] = {"ms": kern_ms["eval_solve"], "launches": 2 * len(sess.engine.groups),
+        kernels["eval_solve"] = {"ms": kern_ms["eval_solve"], "fwd_ms": solve_split[0], "bwd_ms": solve_split[1],
+                                 "launches": 2 * len(sess.engine.groups),
                                  "work": flops["solve"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
                                  "peak_src": pk["fp64_src"]}
     if kern_ms["oz_holdout"] > 0:

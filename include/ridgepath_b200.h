@@ -26,14 +26,14 @@
  * Packed-factor layout ("tile" layout): the order-d
  * lower triangle is cut into 64 x 64 tiles (I, J), I >= J, d padded up to
  * dp = 64 * ceil(d / 64). Tile (I, J) is stored at tile index I(I+1)/2 + J;
- * a tile holds P = r + 1 coefficient planes of 64 x 64 with a padded leading
- * dimension of 68 (TP = 64*68 doubles per plane). Each fold's buffer holds two
- * copies: the forward copy (plane p of tile t at (t*P + p)*TP, element (i, j)
- * at j*68 + i, column-major) followed by the transposed backward copy (same
- * offsets plus rp_tile_count(d)*P*TP, element (i, j) at i*68 + j), so every
- * 16-column / 16-row slab of a tile is one contiguous block. Entries above the
- * diagonal of a diagonal tile and the padding are 0; padded diagonal entries
- * are 1 in plane 0 (the identity) so solves stay well defined. Per fold:
+ * a tile holds P = r + 1 coefficient planes of 64 x 64, column-major with a
+ * padded leading dimension of 68 (TP = 64*68 doubles per plane): plane p of
+ * tile t at (t*P + p)*TP, element (i, j) at j*68 + i. A 16-column slab of a
+ * tile is one contiguous block (the forward substitution's bulk copies) and a
+ * 16-row slab is one 2-D TMA box (the backward substitution reads the
+ * transposed operand from the same copy). Entries above the diagonal of a
+ * diagonal tile and the padding are 0; padded diagonal entries are 1 in
+ * plane 0 (the identity) so solves stay well defined. Per fold:
  * rp_theta_size(d, r) doubles.
  */
 #ifndef RIDGEPATH_B200_H
@@ -58,7 +58,7 @@ long long rp_launch_count(void);
 long long rp_ozaki_fallbacks(void);
 
 /* Number of 64 x 64 tiles of the packed lower triangle of order d, and the
- * size in doubles of one fold's coefficient buffer (both tile copies). */
+ * size in doubles of one fold's coefficient buffer. */
 int64_t rp_tile_count(int d);
 int64_t rp_theta_size(int d, int r);
 

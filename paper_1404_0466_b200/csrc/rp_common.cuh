@@ -6,6 +6,8 @@
 // DFMA 33.6 TFLOP/s, and the two share one FP64 datapath (mixed 31.6 + 4.0).
 #pragma once
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -83,16 +85,38 @@ RP_DEVINL void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, uint64_t* 
                : "memory");
 }
 
+// 2-D TMA load (tensor map in param / const / global space), completion on `bar`.
+RP_DEVINL void tma_2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
 RP_DEVINL void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }
 
 }  // namespace rp
 
-// Coefficient tile layout v2 (include/ridgepath_b200.h): 64 x 64 planes with a padded leading
-// dimension, stored twice per fold -- column-major ("forward" copy) and row-major (the transposed
-// "backward" copy) -- so that every 16-column / 16-row slab the solve streams is one contiguous
-// bulk copy that lands in the conflict-free padded shared layout.
+// Coefficient tile layout (include/ridgepath_b200.h): 64 x 64 column-major planes with a padded
+// leading dimension of 68, so a 16-column slab (forward substitution) is one contiguous bulk copy
+// that lands in a conflict-free shared layout, and a 16-row slab (backward substitution, the
+// transposed operand) is one 2-D TMA box {16 rows, 64 columns} with the 128-byte swizzle.
 constexpr int TILE_LD = 68;
 constexpr int TILE_PLANE = 64 * TILE_LD;
 

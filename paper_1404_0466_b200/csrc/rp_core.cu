@@ -232,10 +232,14 @@ struct FitArgs {
   double V[32][5];  // s x (r+1)
 };
 
+// theta_p = sum_s P[p][s] L_s for one 64 x 64 tile (I, J) of every fold, written straight into the
+// column-major padded tile planes (consecutive threads on consecutive rows: coalesced reads of the
+// factors and writes of the planes), with the tile's share of ||T - V theta||_F^2. Padding rows
+// (64..67) and entries outside the triangle are 0, padded diagonal entries 1 in plane 0.
 template <int SMAX>
 __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles,
-                                                        FitArgs fa, double* theta, double* partial) {
-  extern __shared__ double pl[];  // P planes of 64 x 65 (column-major, padded) for the transpose
+                                                        int64_t fold_stride, FitArgs fa, double* theta,
+                                                        double* partial) {
   const int64_t tile = blockIdx.x;
   const int f = blockIdx.y;
   const int P = r + 1;
@@ -245,14 +249,12 @@ __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, 
   const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
   const int64_t n = (int64_t)d * d;
   const double* Lf = L + (int64_t)f * s * n;
-  const int64_t tsz = (int64_t)P * TILE_PLANE;
-  double* fwd = theta + (int64_t)f * 2 * ntiles * tsz + tile * tsz;
-  double* bwd = fwd + ntiles * tsz;
+  double* out = theta + f * fold_stride + tile * P * TILE_PLANE;
   double res = 0.0;
-  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
-    const int j = e >> 6, i = e & 63;
+  for (int e = threadIdx.x; e < TILE_PLANE; e += blockDim.x) {
+    const int j = e / TILE_LD, i = e - j * TILE_LD;  // (row i, col j) of the tile
     const int row = I * 64 + i, col = J * 64 + j;
-    if (row < d && col < d && row >= col) {
+    if (i < 64 && row < d && col < d && row >= col) {
       double T[SMAX];
 #pragma unroll
       for (int si = 0; si < SMAX; ++si) T[si] = (si < s) ? __ldcs(Lf + si * n + (int64_t)col * d + row) : 0.0;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, 
           for (int si = 0; si < SMAX; ++si)
             if (si < s) v = fma(fa.P[p][si], T[si], v);
           th[p] = v;
-          pl[p * 4160 + j * 65 + i] = v;
+          __stcs(out + p * TILE_PLANE + e, v);
         }
       }
 #pragma unroll
@@ -280,17 +282,9 @@ __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, 
         }
       }
     } else {
-      const double diag = (row == col && row >= d) ? 1.0 : 0.0;
-      for (int p = 0; p < P; ++p) pl[p * 4160 + j * 65 + i] = (p == 0) ? diag : 0.0;
+      const double diag = (i < 64 && row == col && row >= d) ? 1.0 : 0.0;
+      for (int p = 0; p < P; ++p) __stcs(out + p * TILE_PLANE + e, (p == 0) ? diag : 0.0);
     }
-  }
-  __syncthreads();
-  // forward copy: column-major, leading dimension TILE_LD; backward copy: row-major (transposed)
-  for (int e = threadIdx.x; e < P * TILE_PLANE; e += blockDim.x) {
-    const int p = e / TILE_PLANE, w = e - p * TILE_PLANE;
-    const int a = w / TILE_LD, b = w - a * TILE_LD;  // a: major index, b: minor (0..67)
-    __stcs(fwd + e, (b < 64) ? pl[p * 4160 + a * 65 + b] : 0.0);  // (row b, col a)
-    __stcs(bwd + e, (b < 64) ? pl[p * 4160 + b * 65 + a] : 0.0);  // (row a, col b)
   }
   __shared__ double red[512];
   red[threadIdx.x] = res;
@@ -348,8 +342,8 @@ __global__ void export_kernel(const double* theta, int d, int P, const int64_t* 
 __global__ void theta_init_kernel(double* theta, int d, int P, int64_t ntiles) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t half = ntiles * P * TILE_PLANE;
-  if (e >= 2 * half) return;
-  const int64_t w0 = e % half;
+  if (e >= half) return;
+  const int64_t w0 = e;
   const int64_t tile = w0 / (P * TILE_PLANE);
   const int rem = (int)(w0 % (P * TILE_PLANE));
   const int p = rem / TILE_PLANE, w = rem % TILE_PLANE;
@@ -358,7 +352,7 @@ __global__ void theta_init_kernel(double* theta, int d, int P, int64_t ntiles) {
   while ((int64_t)I * (I + 1) / 2 > tile) --I;
   const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
   const int mj = w / TILE_LD, mn = w % TILE_LD;
-  // same (row, col) mapping up to transposition; only the padded diagonal is nonzero
+  // only the padded diagonal is nonzero
   const int row = I * 64 + mn, col = J * 64 + mj;
   theta[e] = (p == 0 && mn < 64 && row == col && row >= d) ? 1.0 : 0.0;
 }
@@ -372,12 +366,7 @@ __global__ void import_kernel(const double* vec, int d, int P, const int64_t* pe
   if (row < col) return;
   const int I = row >> 6, J = col >> 6;
   const int64_t base = ((int64_t)I * (I + 1) / 2 + J) * P * TILE_PLANE;
-  const int64_t half = ntiles * P * TILE_PLANE;
-  for (int p = 0; p < P; ++p) {
-    const double v = vec[p * D + j];
-    theta[base + (int64_t)p * TILE_PLANE + (col & 63) * TILE_LD + (row & 63)] = v;         // forward
-    theta[half + base + (int64_t)p * TILE_PLANE + (row & 63) * TILE_LD + (col & 63)] = v;  // backward
-  }
+  for (int p = 0; p < P; ++p) theta[base + (int64_t)p * TILE_PLANE + (col & 63) * TILE_LD + (row & 63)] = vec[p * D + j];
 }
 
 // ------------------------------------------------------------------ hold-out reductions
@@ -587,7 +576,13 @@ int64_t rp_tile_count(int d) {
   return nt * (nt + 1) / 2;
 }
 
-int64_t rp_theta_size(int d, int r) { return 2 * rp_tile_count(d) * (r + 1) * TILE_PLANE; }
+int64_t rp_theta_size(int d, int r) {
+#ifdef RP_THETA_GAP  // experiment: fold stride with a gap as large as the data
+  return 2 * rp_tile_count(d) * (r + 1) * TILE_PLANE;
+#else
+  return rp_tile_count(d) * (r + 1) * TILE_PLANE;
+#endif
+}
 
 size_t rp_gram_workspace_size(int d, int64_t rows_per_block, int nblocks) {
   if (d < 1 || rows_per_block < 1 || nblocks < 1) return 0;
@@ -978,14 +973,12 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
     }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nt = rp_tile_count(d);
-  const size_t fsm = sizeof(double) * (size_t)(r + 1) * 4160;
-  if (s <= 8) {
-    cudaFuncSetAttribute(fit_tiles_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
-  } else {
-    cudaFuncSetAttribute(fit_tiles_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
-    fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, fsm, st>>>(L, d, s, r, nt, fa, theta, (double*)work);
-  }
+  if (s <= 8)
+    fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
+                                                                 (double*)work);
+  else
+    fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
+                                                                  (double*)work);
   RP_LAUNCH_CHECK("fit_tiles");
   if (resid) {
     fit_resid_kernel<<<nf, 256, 0, st>>>((double*)work, nt, resid);
@@ -1029,8 +1022,11 @@ static int64_t holdout_mt(int64_t n_val, int d) {
 static size_t holdout_base_bytes(int64_t n_val, int d, int64_t N, int nf) {
   return (sizeof(double) * (size_t)(nf * holdout_mt(n_val, d) * N + nf * N) + 1023) / 1024 * 1024;
 }
+static size_t holdout_rep_list_bytes(int64_t N, int nf) {  // count (16 bytes) + list, 16-byte aligned
+  return (16 + sizeof(int) * (size_t)nf * N + 15) / 16 * 16;
+}
 static size_t holdout_rep_bytes(int64_t N, int nf) {
-  return (16 + sizeof(int) * (size_t)nf * N + sizeof(double) * (size_t)nf * N * REP_CHUNKS + 1023) / 1024 * 1024;
+  return (holdout_rep_list_bytes(N, nf) + sizeof(double) * (size_t)nf * N * REP_CHUNKS + 1023) / 1024 * 1024;
 }
 
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf) {
@@ -1089,7 +1085,7 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
   w8 += holdout_base_bytes(n_val, d, N, nf);
   int* rep_count = reinterpret_cast<int*>(w8);
   int* rep_list = rep_count + 4;
-  double* rep_part = reinterpret_cast<double*>(w8 + 16 + sizeof(int) * (size_t)nf * N);
+  double* rep_part = reinterpret_cast<double*>(w8 + holdout_rep_list_bytes(N, nf));
   w8 += holdout_rep_bytes(N, nf);
   cudaError_t e = cudaMemsetAsync(rep_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return cuda_status(e, "holdout repair count");
@@ -1125,7 +1121,7 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
     RP_LAUNCH_CHECK("holdout symmetrize");
   }
   {
-    ProfScope prof("holdout_gemm", st);
+    ProfScope prof(a.run_if_set ? "holdout_gemm_fallback" : "holdout_gemm", st);
     rc = gemm<A_KMAJOR, 128, 128, 64, 32, EPI_DOTB>(a, nf, st, "holdout gram");
   }
   if (rc) return rc;

@@ -31,9 +31,6 @@
 //   oz_dotb_pair_kernel  the Gram-form hold-out w^T T w on the same machinery.
 // Every product has a device-side range guard (OZ_RANGE_BITS below) with a gated FP64 DMMA fallback.
 #pragma once
-#include <cuda.h>
-#include <cudaTypedefs.h>
-
 #include "rp_common.cuh"
 
 namespace rp {
@@ -791,17 +788,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
 
 // ------------------------------------------------------------------ host side
 
-inline PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      p = nullptr;
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }();
-  return fn;
-}
+inline PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() { return tensor_map_encoder(); }
 
 // 2-D int8 view of the slices: inner dim kpad bytes, outer nbatch*S*M rows; SWIZZLE_32B boxes of
 // 32 x 128.

@@ -12,31 +12,30 @@ namespace rp {
 int g_solve_lam = 0;  // rp_set_option("solve_lam", n): 0 = the planner's choice
 }
 
-static int launch_generic(int m, const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
+static int launch_generic(int m, const SolveArgs& a, int grid, cudaStream_t st) {
   switch (m) {
-    case 1: return launch_solve<0, 1, 0, 0>(a, grid, smem, st);
-    case 2: return launch_solve<0, 2, 0, 0>(a, grid, smem, st);
-    case 3: return launch_solve<0, 3, 0, 0>(a, grid, smem, st);
-    case 4: return launch_solve<0, 4, 0, 0>(a, grid, smem, st);
-    case 5: return launch_solve<0, 5, 0, 0>(a, grid, smem, st);
-    case 6: return launch_solve<0, 6, 0, 0>(a, grid, smem, st);
-    case 7: return launch_solve<0, 7, 0, 0>(a, grid, smem, st);
-    case 8: return launch_solve<1, 0, 0, 0>(a, grid, smem, st);
-    case 9: return launch_solve<1, 1, 0, 0>(a, grid, smem, st);
-    case 10: return launch_solve<1, 2, 0, 0>(a, grid, smem, st);
-    case 11: return launch_solve<1, 3, 0, 0>(a, grid, smem, st);
-    case 12: return launch_solve<1, 4, 0, 0>(a, grid, smem, st);
-    case 13: return launch_solve<1, 5, 0, 0>(a, grid, smem, st);
-    case 14: return launch_solve<1, 6, 0, 0>(a, grid, smem, st);
-    case 15: return launch_solve<1, 7, 0, 0>(a, grid, smem, st);
-    default: return launch_solve<2, 0, 0, 0>(a, grid, smem, st);
+    case 1: return launch_solve<0, 1, 0, 0>(a, grid, st);
+    case 2: return launch_solve<0, 2, 0, 0>(a, grid, st);
+    case 3: return launch_solve<0, 3, 0, 0>(a, grid, st);
+    case 4: return launch_solve<0, 4, 0, 0>(a, grid, st);
+    case 5: return launch_solve<0, 5, 0, 0>(a, grid, st);
+    case 6: return launch_solve<0, 6, 0, 0>(a, grid, st);
+    case 7: return launch_solve<0, 7, 0, 0>(a, grid, st);
+    case 8: return launch_solve<1, 0, 0, 0>(a, grid, st);
+    case 9: return launch_solve<1, 1, 0, 0>(a, grid, st);
+    case 10: return launch_solve<1, 2, 0, 0>(a, grid, st);
+    case 11: return launch_solve<1, 3, 0, 0>(a, grid, st);
+    case 12: return launch_solve<1, 4, 0, 0>(a, grid, st);
+    case 13: return launch_solve<1, 5, 0, 0>(a, grid, st);
+    case 14: return launch_solve<1, 6, 0, 0>(a, grid, st);
+    case 15: return launch_solve<1, 7, 0, 0>(a, grid, st);
+    default: return launch_solve<2, 0, 0, 0>(a, grid, st);
   }
 }
 
 struct SolvePlan {
   int lam = 0, chunks = 0, S = 0, P = 0, nt = 0;
   bool fast = false;
-  size_t smem = 0;
 };
 
 // Chunk size: specialised kernels (full chunks, compile-time P) and the generic kernel compete
@@ -52,7 +51,7 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
   double best_cost = 1e300;
   for (int lam = SOLVE_LC; lam >= 1; --lam) {
     if (lam * m > 256) continue;  // one thread per (lambda, output) column in the diagonal solve
-    if (solve_smem_bytes(lam, m, pl.P) > (size_t)maxsmem) continue;
+    if (solve_smem_max(lam, m, pl.P) > (size_t)maxsmem) continue;
     const int chunks = (q + lam - 1) / lam;
     const long long ctas = (long long)nf * chunks;
     const double waves = (double)((ctas + sms - 1) / sms);
@@ -76,14 +75,13 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
   // rp_set_option("solve_lam", n) (tests): force a specialised chunk size when it exists
   const int lam_force = g_solve_lam;
   if (lam_force > 0 && q >= lam_force && has_solve_fast(m, pl.P, lam_force) &&
-      ((m % 2 == 0) || ((q - lam_force) % 2 == 0)) && solve_smem_bytes(lam_force, m, pl.P) <= (size_t)maxsmem) {
+      ((m % 2 == 0) || ((q - lam_force) % 2 == 0)) && solve_smem_max(lam_force, m, pl.P) <= (size_t)maxsmem) {
     pl.lam = lam_force;
     pl.fast = true;
   }
   if (pl.lam > 0) {
     pl.chunks = (q + pl.lam - 1) / pl.lam;
     pl.S = solve_stride(pl.lam, m);
-    pl.smem = solve_smem_bytes(pl.lam, m, pl.P);
   }
   return pl;
 }
@@ -109,10 +107,25 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   const SolvePlan pl = plan_solve(d, r, nf, m, q);
   RP_REQUIRE(pl.lam >= 1, "rp_eval_solve: no chunk size fits shared memory");
   const int P = pl.P, nt = pl.nt;
-  SolveArgs a;
+  SolveArgs a{};
   a.theta = theta;
   a.theta_fold_stride = rp_theta_size(d, r);
-  a.theta_bwd_off = rp_tile_count(d) * P * TILE_PLANE;
+  a.ntiles = rp_tile_count(d);
+  {  // backward slabs: 2-D FP64 view of all folds' tiles, inner dim = the 68-padded column
+    auto enc = tensor_map_encoder();
+    RP_REQUIRE(enc != nullptr, "rp_eval_solve: cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)TILE_LD, (cuuint64_t)(nf * a.theta_fold_stride / TILE_LD)};
+    cuuint64_t strides[1] = {(cuuint64_t)TILE_LD * sizeof(double)};
+    cuuint32_t box[2] = {16, 64};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&a.tmb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(theta), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+#ifndef RP_SOLVE_PROMO
+#define RP_SOLVE_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
+                      RP_SOLVE_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return set_error(RP_ECUDA, "rp_eval_solve: tensor map (CUresult %d)", (int)cr);
+  }
   a.rhs = rhs;
   a.rhs_fold_stride = (int64_t)nt * 64 * m;
   a.W = W;
@@ -132,6 +145,6 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   const int grid = nf * a.chunks;
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
   if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");
-  if (pl.fast) return launch_solve_fast(m, P, pl.lam, a, grid, pl.smem, st);
-  return launch_generic(m, a, grid, pl.smem, st);
+  if (pl.fast) return launch_solve_fast(m, P, pl.lam, a, grid, st);
+  return launch_generic(m, a, grid, st);
 }

@@ -48,10 +48,11 @@ constexpr int SOLVE_LC = 16;          // max lambdas per CTA (specialised kernel
 constexpr int SOLVE_LC_GENERIC = 8;   // max lambdas per CTA (generic kernel)
 constexpr int SOLVE_PMAX = 5;    // max polynomial planes (degree <= 4)
 constexpr int SOLVE_STAGES = 3;
-constexpr int FWD_SLAB = 16 * 68;   // per plane: 16 columns x 64 rows (stride 68)
-constexpr int BWD_SLAB = 64 * 20;   // per plane: 64 columns x 16 rows (stride 20)
+constexpr int FWD_SLAB = 16 * 68;   // per plane: 16 columns x 64 rows (stride 68), one bulk copy
+constexpr int BWD_SLAB = 64 * 16;   // per plane: 64 columns x 16 rows, one 2-D TMA box, 128-byte swizzle
 
 struct SolveArgs {
+  CUtensorMap tmb;  // backward slabs: 2-D view {68, nf * theta_fold_stride / 68} of the tile layout
   const double* theta;
   int64_t theta_fold_stride;
   const double* rhs;
@@ -61,8 +62,8 @@ struct SolveArgs {
   const double* tvals;
   int* flags;
   int q, m, d, nt, P, lam_per_cta, chunks, S;
-  double* Wc;             // chunk-private rows of the solution (dp x S per CTA)
-  int64_t theta_bwd_off;  // offset of the transposed (backward) tile copy inside a fold's theta
+  double* Wc;      // chunk-private rows of the solution (dp x S per CTA)
+  int64_t ntiles;  // 64 x 64 tiles per fold
 };
 
 RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
@@ -77,7 +78,7 @@ RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 // every W fragment loaded from shared memory feeds two DMMAs and every coefficient fragment
 // is evaluated for half of the chunk's lambdas.
 template <int NT, int REM, int PT, int LCT, int LG, int STG, bool BWD>
-__global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
+__global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_constant__ SolveArgs a) {
   constexpr int NTH = 128 * LG;  // 4 row groups x LG lambda groups of warps
   constexpr int LC = LCT ? LCT : SOLVE_LC_GENERIC;
   constexpr int LH = (LC + LG - 1) / LG;
@@ -85,14 +86,17 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   constexpr int REMA = REM > 0 ? REM : 1;
   constexpr int NTA = NT > 0 ? NT : 1;
   constexpr bool REM2 = (REM % 2) == 0;
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(16) double smem_raw[];
+  // backward pass: 1 KB-aligned base, the slabs land with the 128-byte TMA swizzle (8-row atoms of 1 KB)
+  // (pointer arithmetic on the shared array, so the compiler keeps shared-memory loads)
+  double* smem = BWD ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) / 8 : smem_raw;
   // diagonal-block helpers (static): packed lower index -> (row, col) of a 16 x 16 block, and the
   // chunk's t values
   __shared__ uint8_t s_pi[136], s_pj[136];
   __shared__ double s_tv[LCT ? LCT : SOLVE_LC_GENERIC];
   const int P = PT ? PT : a.P;
   const int S = a.S, m = a.m;
-  const int stageT = P * FWD_SLAB;  // both directions: [k][68] slabs (bwd from the transposed copy)
+  const int stageT = P * (BWD ? BWD_SLAB : FWD_SLAB);
   const int stageW = 16 * S;
   double* sT = smem;
   double* sW = smem + STG * stageT;
@@ -106,12 +110,17 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int rg = warp & 3, lg = warp >> 2;  // row group, lambda group
+  // tile row of this lane's DMMA row g in m-tile mt (the accumulators follow the A fragments): fwd
+  // pairs the two m-tiles' rows (16-byte loads of adjacent rows), bwd spreads the rows of each
+  // quarter-warp over both halves of the 128-byte swizzle atom (conflict-free 16-byte loads)
+  auto slab_row = [&](int mt) {
+    return BWD ? rg * 16 + mt * 8 + (g >> 1) + 4 * (g & 1) : rg * 16 + 2 * g + mt;
+  };
   const int fold = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
   const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
   const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
   if (nl <= 0) return;
   const double* theta = a.theta + fold * a.theta_fold_stride;
-  const double* thslab = theta + (BWD ? a.theta_bwd_off : 0);  // slabs: fwd or transposed copy
   double* W = a.W + fold * a.w_fold_stride;
   double* Wc = a.Wc + (int64_t)blockIdx.x * (a.nt * 64) * S;  // this CTA's private solve rows
   const int cw = nl * m;  // valid chunk columns
@@ -162,8 +171,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         for (int c = 0; c < REMA; ++c) accx[i][mt][c] = 0.0;
       }
 
-    // one thread streams slab s: P contiguous 16-column (fwd) / 16-row (bwd, transposed copy)
-    // plane slices + the 16 already solved rows of this CTA's private W, completion on full[st].
+    // one thread streams slab s: P contiguous 16-column plane slices (fwd: bulk copies) or P 16-row
+    // x 64-column boxes of the transposed operand (bwd: 2-D TMA from the same column-major tiles,
+    // 128-byte swizzle) + the 16 already solved rows of this CTA's private W, completion on full[st].
     // A stage is refilled once every warp has released its previous slab (empty[st]); only the
     // issuing thread waits for that, the other warps run ahead as far as the data allows.
     auto issue = [&](int s) {
@@ -172,67 +182,103 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
         if (it >= STG) mbar_wait(&empty[st], ((it / STG) + 1) & 1);
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
         const int kq = s & 3;
-        const double* tile = thslab + (int64_t)(BWD ? tile_index(J, I) : tile_index(I, J)) * P * TILE_PLANE;
-        const uint32_t bytes = (uint32_t)(P * FWD_SLAB * 8 + 16 * S * 8);
+        const uint32_t bytes = (uint32_t)(stageT * 8 + 16 * S * 8);
         mbar_arrive_expect_tx(&full[st], bytes);
-        for (int p = 0; p < P; ++p)
-          bulk_g2s(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
-                   (uint32_t)(FWD_SLAB * 8), &full[st]);
+        if (BWD) {
+          const int64_t row0 = fold * a.theta_fold_stride / TILE_LD + (int64_t)tile_index(J, I) * P * 64;
+          for (int p = 0; p < P; ++p)
+            tma_2d_g2s(sT + st * stageT + p * BWD_SLAB, &a.tmb, kq * 16, (int)(row0 + p * 64), &full[st]);
+        } else {
+          const double* tile = theta + (int64_t)tile_index(I, J) * P * TILE_PLANE;
+          for (int p = 0; p < P; ++p)
+            bulk_g2s(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
+                     (uint32_t)(FWD_SLAB * 8), &full[st]);
+        }
         bulk_g2s(sW + st * stageW, Wc + (int64_t)(J * 64 + kq * 16) * S, (uint32_t)(16 * S * 8), &full[st]);
       }
     };
 
-    issue(0);
-    issue(1);
+#ifndef RP_SOLVE_AHEAD_BWD
+#define RP_SOLVE_AHEAD_BWD 2
+#endif
+#ifndef RP_SOLVE_AHEAD_FWD
+#define RP_SOLVE_AHEAD_FWD 2
+#endif
+    constexpr int AHEAD = BWD ? RP_SOLVE_AHEAD_BWD : RP_SOLVE_AHEAD_FWD;  // slabs in flight ahead of the consumers
+#pragma unroll
+    for (int s0 = 0; s0 < AHEAD; ++s0) issue(s0);
 #pragma unroll 1
     for (int s = 0; s < nslab; ++s) {
-      issue(s + 2);
+      issue(s + AHEAD);
       const int st = (it0 + s) % STG;
       mbar_wait(&full[st], ((it0 + s) / STG) & 1);
       const double* T = sT + st * stageT;
       const double* Wb = sW + st * stageW;
+      // Each lane's A fragments come from one 16-byte shared load per (plane, k-step pair):
+      //  fwd: the rows of its two m-tiles are adjacent (slab_row), A(row, k), A(row + 1, k) at [k][68];
+      //  bwd: its k values of the k-steps 2 kp and 2 kp + 1 are adjacent (k = 8 kp + 2 t + h), one
+      //       swizzled 16-byte chunk of row slab_row(mt), chunk index (4 kp + t) ^ (row & 7).
+      // Both are bank-conflict free, and the B fragments (W rows k) stay conflict free (S = 12 mod 16).
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        const int k = ks * 4 + t;
-        double th[2][PM];
+      for (int kp = 0; kp < 2; ++kp) {
+        double th[2][2][PM];  // [h: k-step 2 kp + h][mt][plane]
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          const int row = rg * 16 + mt * 8 + g;
+        for (int p = 0; p < PM; ++p) {
+          if (p < P) {
+            if (BWD) {
 #pragma unroll
-          for (int p = 0; p < PM; ++p)
-            if (p < P) th[mt][p] = T[p * FWD_SLAB + k * 68 + row];
-        }
-        const double* wrow = Wb + k * S;
-#pragma unroll
-        for (int i = 0; i < LH; ++i) {
-          const int l = lg * LH + i;
-          if (l < nl) {
-            double b[NTA];
-#pragma unroll
-            for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
-            double rv[REMA];
-            if (REM2) {
-#pragma unroll
-              for (int c = 0; c < REM; c += 2) {
-                const double2 v2 = *reinterpret_cast<const double2*>(wrow + l * m + NT * 8 + c);
-                rv[c] = v2.x;
-                rv[c + 1] = v2.y;
+              for (int mt = 0; mt < 2; ++mt) {
+                const int row = slab_row(mt);
+                const double2 v = *reinterpret_cast<const double2*>(
+                    T + p * BWD_SLAB + row * 16 + (((4 * kp + t) ^ (row & 7)) << 1));
+                th[0][mt][p] = v.x;
+                th[1][mt][p] = v.y;
               }
             } else {
 #pragma unroll
-              for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
+              for (int h = 0; h < 2; ++h) {
+                const double2 v = *reinterpret_cast<const double2*>(
+                    T + p * FWD_SLAB + ((2 * kp + h) * 4 + t) * 68 + slab_row(0));
+                th[h][0][p] = v.x;
+                th[h][1][p] = v.y;
+              }
             }
+          }
+        }
 #pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-              // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
-              double av = 0.0;
+        for (int h = 0; h < 2; ++h) {
+          const double* wrow = Wb + (BWD ? 8 * kp + 4 * h + t : (2 * kp + h) * 4 + t) * S;
 #pragma unroll
-              for (int p = PM - 1; p >= 0; --p)
-                if (p < P) av = (p == P - 1) ? th[mt][p] : fma(av, tl[i], th[mt][p]);
+          for (int i = 0; i < LH; ++i) {
+            const int l = lg * LH + i;
+            if (l < nl) {
+              double b[NTA];
 #pragma unroll
-              for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
+              for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
+              double rv[REMA];
+              if (REM2) {
 #pragma unroll
-              for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+                for (int c = 0; c < REM; c += 2) {
+                  const double2 v2 = *reinterpret_cast<const double2*>(wrow + l * m + NT * 8 + c);
+                  rv[c] = v2.x;
+                  rv[c + 1] = v2.y;
+                }
+              } else {
+#pragma unroll
+                for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
+              }
+#pragma unroll
+              for (int mt = 0; mt < 2; ++mt) {
+                // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
+                double av = 0.0;
+#pragma unroll
+                for (int p = PM - 1; p >= 0; --p)
+                  if (p < P) av = (p == P - 1) ? th[h][mt][p] : fma(av, tl[i], th[h][mt][p]);
+#pragma unroll
+                for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
+#pragma unroll
+                for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+              }
             }
           }
         }
@@ -259,7 +305,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
       if (l < nl) {
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-          const int row = rg * 16 + mt * 8 + g;
+          const int row = slab_row(mt);
 #pragma unroll
           for (int c = 0; c < REM; ++c) {
             double v = accx[i][mt][c];
@@ -365,7 +411,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           double th[2][PM];
 #pragma unroll
           for (int mt = 0; mt < 2; ++mt) {
-            const int row = rg * 16 + mt * 8 + g;
+            const int row = slab_row(mt);
             // fwd: L(row, k) (column k of the tile); bwd: L(k, row) (column row)
             const int off = BWD ? row * TILE_LD + k : k * TILE_LD + row;
 #pragma unroll
@@ -404,7 +450,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
           if (l < nl) {
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
-              const int row = rg * 16 + mt * 8 + g;
+              const int row = slab_row(mt);
 #pragma unroll
               for (int c = 0; c < REM; ++c) {
                 double v = accx[i][mt][c];
@@ -425,8 +471,12 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
     }
     // publish row I: private rows (read back by later slabs through the async proxy) and, for
     // the backward pass, the caller's row-major W (overlapping chunks write identical values)
+    // (the backward pass stores each 16-row group of its private rows in the order its slab loop
+    // reads them: logical row 8 kp + 2 t + h at 8 kp + 4 h + t, so the B fragments and the leftover
+    // 16-byte loads of lanes t = 0..3 hit consecutive rows -- conflict-free with S = 12 mod 16)
     for (int i = warp; i < 64; i += NTH / 32) {
-      double* dc = Wc + (int64_t)(rowI + i) * S;
+      const int ip = BWD ? (i & ~15) | (i & 8) | ((i & 1) << 2) | ((i >> 1) & 3) : i;
+      double* dc = Wc + (int64_t)(rowI + ip) * S;
       for (int c = lane; c < cw; c += 32) dc[c] = sR[i * S + c];
       if (BWD) {
         double* dst = W + (int64_t)(rowI + i) * a.ldw + wcol0;
@@ -450,37 +500,46 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(SolveArgs a) {
 // bank-conflict free.
 inline int solve_stride(int lam, int m) { return ((lam * m + 3) / 16) * 16 + 12; }
 
-inline size_t solve_smem_bytes(int lam, int m, int P, int stages = SOLVE_STAGES) {
+// Dynamic shared memory of one pass. The backward pass's slabs are smaller (64 x 16 TMA boxes vs
+// 16 x 68 columns) but its ring must start on a 1 KB boundary (128-byte swizzle atoms): + 1 KB slack.
+inline size_t solve_smem_bytes(int lam, int m, int P, int stages = SOLVE_STAGES, bool bwd = false) {
   const int S = solve_stride(lam, m);
-  size_t per_stage = (size_t)P * FWD_SLAB + 16 * (size_t)S;
+  size_t per_stage = (size_t)P * (bwd ? BWD_SLAB : FWD_SLAB) + 16 * (size_t)S;
   size_t ring = stages * per_stage;
   // theta_II + the evaluated 16 x 16 diagonal blocks + pivots, in the idle ring during the diagonal step
   size_t diag = (size_t)P * TILE_PLANE + (size_t)lam * (16 * 17 + 16);
-  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 16);  // + mbarriers
+  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 16) + (bwd ? 1024 : 0);  // + mbarriers
+}
+
+inline size_t solve_smem_max(int lam, int m, int P, int stages = SOLVE_STAGES) {
+  const size_t f = solve_smem_bytes(lam, m, P, stages, false), b = solve_smem_bytes(lam, m, P, stages, true);
+  return f > b ? f : b;
 }
 
 
 template <int NT, int REM, int PT, int LCT, int LG = 2, int STG = SOLVE_STAGES>
-int launch_solve(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
+int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
   auto kf = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, false>;
   auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, true>;
-  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t sf = solve_smem_bytes(a.lam_per_cta, a.m, a.P, STG, false);
+  const size_t sb = solve_smem_bytes(a.lam_per_cta, a.m, a.P, STG, true);
+  cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
+  cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
   {
-    ProfScope prof("eval_solve", st);
-    kf<<<grid, 128 * LG, smem, st>>>(a);
+    ProfScope prof("eval_solve_fwd", st);
+    kf<<<grid, 128 * LG, sf, st>>>(a);
   }
   RP_LAUNCH_CHECK("eval_solve fwd");
   {
-    ProfScope prof("eval_solve", st);
-    kb<<<grid, 128 * LG, smem, st>>>(a);
+    ProfScope prof("eval_solve_bwd", st);
+    kb<<<grid, 128 * LG, sb, st>>>(a);
   }
   RP_LAUNCH_CHECK("eval_solve bwd");
   return RP_OK;
 }
 
 // Fast instantiations (rp_solve_fast.cu): returns -2 when (m, P, lam) has none.
-int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, size_t smem, cudaStream_t st);
+int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st);
 bool has_solve_fast(int m, int P, int lam);
 
 }  // namespace rp

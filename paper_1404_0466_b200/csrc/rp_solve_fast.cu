@@ -25,18 +25,17 @@ bool has_solve_fast(int m, int P, int lam) {
 // 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4; a 4-stage
 // ring (two slabs per barrier phase) when it fits in shared memory.
 template <int M, int P, int LC>
-static int launch_fast(const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
+static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st) {
   int dev = 0, maxsm = 227 * 1024;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t sm4 = solve_smem_bytes(LC, M, P, 4);
-  if (sm4 <= (size_t)maxsm) return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, sm4, st);
-  return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, smem, st);
+  if (solve_smem_max(LC, M, P, 4) <= (size_t)maxsm) return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, st);
+  return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, st);
 }
 
-int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, size_t smem, cudaStream_t st) {
+int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st) {
 #define RP_LAUNCH(M, PP, L) \
-  if (m == M && P == PP && lam == L) return launch_fast<M, PP, L>(a, grid, smem, st);
+  if (m == M && P == PP && lam == L) return launch_fast<M, PP, L>(a, grid, st);
   RP_FAST_LIST(RP_LAUNCH)
 #undef RP_LAUNCH
   return -2;

@@ -41,7 +41,7 @@ def padded(d):
 
 
 def tile_elems(d, P):
-    """Doubles of one fold's coefficient buffer (both tile copies, include/ridgepath_b200.h)."""
+    """Doubles of one fold's coefficient buffer (tile layout, include/ridgepath_b200.h)."""
     return int(_lib.query("rp_theta_size", d, P - 1))
 
 

@@ -94,28 +94,40 @@ def test_c4_headline_matches_reference(gpu):
 @pytest.mark.slow
 def test_c5_fold0_matches_reference(gpu):
     """c5 (d = 8192, 16 outputs, cubic with the [-1, 1] rescale), fold 0 x 500 lambdas. The
-    reference's own cubic interpolant collapses near lambda ~ 164..900 (fitted
-    diagonals down to 7e-5, errors up to 1e40): curves are compared where the reference's fitted
-    min |L_ii| is at least 1e-2 (the excluded tail is reported), the argmin everywhere."""
+    reference's own cubic interpolant collapses for lambda > 65 (its fitted
+    min |L_ii| peaks at 8.07 near lambda = 65, then falls to 7e-5 while the exact factor's stays
+    >= 13; curves reach 1e74): there both sides evaluate factors whose conditioning amplifies FP64
+    rounding, and they agree to 1e-9..1e-8 where the collapse starts (grid 440-449) and only ~1e-3 in
+    the blow-up. Curves are compared (north_star tolerance, 1e-8) on the lambdas where the
+    reference's fitted min |L_ii| is at least half its running maximum over smaller lambdas (the
+    interpolant still tracks the factor); the excluded grid indices are reported, with the error on
+    the excluded lambdas whose curve is still within 100x of its minimum."""
     g, cfg, sess, curves, best = run_config("c5")
     ref = g["per_fold"][0]
-    keep = g["mindiag"][0] >= 1e-2
-    mask = np.repeat(keep[:, None], cfg.m, axis=1) & np.isfinite(ref)
+    finite = np.isfinite(ref)
+    md = g["mindiag"][0]
+    keep = (md >= 0.5 * np.maximum.accumulate(md)) & np.all(finite, axis=1)
+    sane = np.all(finite & (ref < 100 * np.min(np.where(finite, ref, np.inf), axis=0)), axis=1)
+    mask = np.repeat(keep[:, None], cfg.m, axis=1)
     err = curve_error(curves[0], ref, mask)
+    per_lam = np.max(np.abs(curves[0] - ref) / np.abs(ref), axis=1)
+    edge = sane & ~keep
     print(f"c5 fold 0: curves max rel err {err:.2e} on {keep.sum()} of {cfg.q} lambdas "
-          f"(excluded grid indices {np.flatnonzero(~keep).tolist()})")
-    assert keep[:400].all() and keep.sum() >= 400
-    assert err <= CURVE_TOL
+          f"(median {np.median(per_lam[keep]):.2e}; excluded grid indices {np.flatnonzero(~keep).tolist()}; "
+          f"max err on the excluded lambdas with a sane curve {np.max(per_lam[edge], initial=0.0):.2e})")
+    assert keep[:440].all() and keep.sum() >= 440
+    assert err <= 1e-8
     # fold 0's own argmins (the selection proper averages 8 folds; the reference's c5 sweep takes ~20
     # CPU-minutes per fold, so only fold 0 is pinned): identical wherever the reference's best-to-second
     # gap exceeds 10x the achieved curve error (output 11's fold-0 gap is 2.5e-11)
-    cref = np.where(np.isfinite(ref), ref, np.inf)
+    cref = np.where(finite, ref, np.inf)
     fold0_best = np.argmin(np.where(np.isfinite(curves[0]), curves[0], np.inf), axis=0)
     ref_best = np.argmin(cref, axis=0)
     srt = np.sort(cref, axis=0)
     gap = (srt[1] - srt[0]) / srt[0]
     resolvable = gap > 10 * err
-    print(f"c5 fold 0: argmins {fold0_best.tolist()} (reference {ref_best.tolist()}); gaps {np.round(gap, 12).tolist()}")
-    assert resolvable.sum() >= 14
+    print(f"c5 fold 0: argmins {fold0_best.tolist()} (reference {ref_best.tolist()}); "
+          f"gaps {[float(f'{v:.2e}') for v in gap]}")
+    assert resolvable.sum() >= 12
     assert np.array_equal(fold0_best[resolvable], ref_best[resolvable])
     check_factors(g, cfg, sess)
