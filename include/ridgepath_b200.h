@@ -91,7 +91,7 @@ int rp_col_sumsq(const double* Y, int64_t ldy, int64_t rows_per_block, int nbloc
 /* Fill the upper triangle of nmat column-major d x d matrices from the lower. */
 int rp_symmetrize(double* G, int d, int64_t stride, int nmat, void* stream);
 
-/* Per-fold shifted systems for the sampled-lambda factorizations
+/* Per-fold shifted systems for the sampled-lambda factorizations (any nf, s: chunked per launch)
  * (pichol.py:105-107, `H + lam * eye`; H = X_tr^T X_tr of ridge.py:58 as a sum of fold blocks):
  *   A[f][s] = sum_{b != folds[f]} G_b + lams[s] * I  (b = 0..nblocks-1 in order; lower triangle,
  *                                                     d x d col-major)
@@ -130,10 +130,12 @@ int rp_potrf_batched(double* A, int d, int64_t stride, int batch, int* info, voi
  * host computed P = (V^T V)^{-1} V^T exactly as the reference (same V, same
  * COND_LIMIT rescale).  Also the Frobenius residual ||T - V theta||_F per fold.
  *   L: nf x s factors (d x d col-major, lower), P: (r+1) x s row-major,
- *   V: s x (r+1) row-major, theta: nf x tile-layout, resid: nf (device)      */
+ *   V: s x (r+1) row-major (host), theta: nf x tile-layout, resid: nf (device).
+ *   Any s > r >= 0 (s <= 32 and r <= 4 keep P and V in kernel parameters; otherwise
+ *   they are copied into the workspace).                                      */
 int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_host,
                  const double* V_host, double* theta, double* resid, void* work, void* stream);
-size_t rp_fit_workspace_size(int d, int nf);
+size_t rp_fit_workspace_size(int d, int nf, int s, int r);
 
 /* (5) Fused evaluate + solve.  Replaces, for all q lambdas at once,
  * pichol.eval_vector (pichol.py:143-151) + trivec.unvectorize
@@ -145,7 +147,9 @@ size_t rp_fit_workspace_size(int d, int nf);
  *   tvals: q values t_j = t_scale*lambda_j + t_shift (device)
  *   W: nf x (dp x ldw) row-major, ldw >= q*m, ldw even
  *   flags: nf x q ints, set to 1 where min |L_ii(t_j)| < 1e-12
- *   work: rp_eval_solve_workspace_size(d, r, nf, m, q) bytes (per-chunk solve rows) */
+ *   work: rp_eval_solve_workspace_size(d, r, nf, m, q) bytes (per-chunk solve rows).
+ *   Degrees up to 4 run fused; a higher degree evaluates each lambda's factor into a
+ *   one-plane tile buffer in the workspace (same Horner arithmetic) and solves it. */
 size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int q);
 int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m, const double* tvals,
                   int q, double* W, int64_t ldw, int* flags, void* work, void* stream);

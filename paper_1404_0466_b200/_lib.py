@@ -46,7 +46,7 @@ SIGNATURES = {
     "rp_potrf_workspace_size": (_sz, [_i, _i]),
     "rp_potrf_batched": (_i, [_vp, _i, _i64, _i, _vp, _vp, _vp]),
     "rp_fit_tiles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "rp_fit_workspace_size": (_sz, [_i, _i]),
+    "rp_fit_workspace_size": (_sz, [_i, _i, _i, _i]),
     "rp_eval_solve_workspace_size": (_sz, [_i, _i, _i, _i, _i]),
     "rp_eval_solve": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i64, _vp, _vp, _vp]),
     "rp_eval_materialize": (_i, [_vp, _i, _i, _d, _vp, _vp]),

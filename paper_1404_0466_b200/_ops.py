@@ -55,7 +55,7 @@ def fit_tiles(L_dev, d, s, nf, r, Pmat, Vmat):
     P = r + 1
     theta = _dev.empty((nf, tile_elems(d, P)))
     resid = _dev.empty((nf,))
-    ws = _dev.workspace(_lib.query("rp_fit_workspace_size", d, nf))
+    ws = _dev.workspace(_lib.query("rp_fit_workspace_size", d, nf, s, r))
     Pm = np.ascontiguousarray(Pmat, dtype=np.float64)
     Vm = np.ascontiguousarray(Vmat, dtype=np.float64)
     call("rp_fit_tiles", ptr(L_dev), d, s, nf, r, _lib.host_ptr(Pm), _lib.host_ptr(Vm), ptr(theta), ptr(resid),

@@ -140,19 +140,22 @@ __global__ void symmetrize_kernel(double* G, int d, int64_t stride) {
   }
 }
 
+constexpr int FS_FOLDS = 64, FS_LAMS = 32;  // per launch; rp_fold_systems chunks over more
 struct FoldSysArgs {
-  int folds[64];
-  double lams[32];
+  int folds[FS_FOLDS];
+  double lams[FS_LAMS];
 };
 
 // Leave-one-out sums, one pass over the Gram blocks for all folds of the call:
-//   A[f][s] = sum_{b != folds[f]} G_b + lams[s] I  (fixed order b = 0..nblocks-1, lower triangle)
+//   A[f][s0 + s] = sum_{b != folds[f]} G_b + lams[s] I  (fixed order b = 0..nblocks-1, lower triangle)
+// A[f] holds s_total matrices (a launch covers lambdas s0 .. s0 + s - 1).
 // Each element's nblocks values are read once (registers when nblocks <= KB) and every fold's sum
 // is formed directly -- no G_total - G_f cancellation, and the sum of a fold is bit-identical
 // whether or not its own block is among the nblocks (the streamed path factors the last fold
 // before its block has arrived). Column by column so the threads of a block stay on contiguous rows.
 template <int KB>
-__global__ void fold_shift_kernel(const double* G, int nblocks, int d, int s, int nf, FoldSysArgs fa, double* A) {
+__global__ void fold_shift_kernel(const double* G, int nblocks, int d, int s, int s0, int s_total, int nf,
+                                  FoldSysArgs fa, double* A) {
   const int j = blockIdx.x;  // column
   const int64_t n = (int64_t)d * d;
   const double* gj = G + (int64_t)j * d;
@@ -173,7 +176,7 @@ __global__ void fold_shift_kernel(const double* G, int nblocks, int d, int s, in
         for (int b = 0; b < nblocks; ++b)
           if (b != hold) v += gj[b * n + i];
       }
-      double* out = A + (int64_t)f * s * n + (int64_t)j * d + i;
+      double* out = A + ((int64_t)f * s_total + s0) * n + (int64_t)j * d + i;
       for (int si = 0; si < s; ++si) __stcs(out + si * n, (i == j) ? v + fa.lams[si] : v);
     }
   }
@@ -284,6 +287,53 @@ __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, 
     } else {
       const double diag = (i < 64 && row == col && row >= d) ? 1.0 : 0.0;
       for (int p = 0; p < P; ++p) __stcs(out + p * TILE_PLANE + e, (p == 0) ? diag : 0.0);
+    }
+  }
+  __shared__ double red[512];
+  red[threadIdx.x] = res;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[(int64_t)f * ntiles + tile] = red[0];
+}
+
+// Any number of samples / planes (s > 32 or degree > 4): the same arithmetic with P (P x s) and V
+// (s x P) in device memory and the samples re-read per plane (L1-resident); not on the BASELINE path.
+__global__ void __launch_bounds__(512) fit_tiles_any_kernel(const double* L, int d, int s, int r, int64_t ntiles,
+                                                            int64_t fold_stride, const double* Pd, const double* Vd,
+                                                            double* theta, double* partial) {
+  const int64_t tile = blockIdx.x;
+  const int f = blockIdx.y;
+  const int P = r + 1;
+  int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
+  while ((int64_t)I * (I + 1) / 2 > tile) --I;
+  const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  const int64_t n = (int64_t)d * d;
+  const double* Lf = L + (int64_t)f * s * n;
+  double* out = theta + f * fold_stride + tile * P * TILE_PLANE;
+  double res = 0.0;
+  for (int e = threadIdx.x; e < TILE_PLANE; e += blockDim.x) {
+    const int j = e / TILE_LD, i = e - j * TILE_LD;
+    const int row = I * 64 + i, col = J * 64 + j;
+    if (i < 64 && row < d && col < d && row >= col) {
+      const double* Le = Lf + (int64_t)col * d + row;
+      for (int p = 0; p < P; ++p) {
+        double v = 0.0;
+        for (int si = 0; si < s; ++si) v = fma(Pd[p * s + si], Le[si * n], v);
+        out[p * TILE_PLANE + e] = v;
+      }
+      for (int si = 0; si < s; ++si) {
+        double v = 0.0;
+        for (int p = 0; p < P; ++p) v = fma(Vd[si * P + p], out[p * TILE_PLANE + e], v);
+        const double dlt = Le[si * n] - v;
+        res = fma(dlt, dlt, res);
+      }
+    } else {
+      const double diag = (i < 64 && row == col && row >= d) ? 1.0 : 0.0;
+      for (int p = 0; p < P; ++p) out[p * TILE_PLANE + e] = (p == 0) ? diag : 0.0;
     }
   }
   __shared__ double red[512];
@@ -723,26 +773,34 @@ int rp_col_sumsq(const double* Y, int64_t ldy, int64_t rows_per_block, int nbloc
 
 int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m, const int* folds_host, int nf,
                     const double* lams_host, int s, double* A, double* rhs, void* stream) {
-  RP_REQUIRE(nf >= 1 && nf <= 64 && s >= 1 && s <= 32, "rp_fold_systems: nf=%d (<=64), s=%d (<=32)", nf, s);
+  RP_REQUIRE(nf >= 1 && s >= 1, "rp_fold_systems: nf=%d, s=%d", nf, s);
   RP_REQUIRE(nblocks >= 1 && d >= 1 && m >= 0, "rp_fold_systems: nblocks=%d d=%d m=%d", nblocks, d, m);
-  FoldSysArgs fa;
-  for (int f = 0; f < nf; ++f) {
-    RP_REQUIRE(folds_host[f] >= -1, "rp_fold_systems: fold %d", folds_host[f]);
-    fa.folds[f] = folds_host[f];
-  }
-  for (int i = 0; i < s; ++i) fa.lams[i] = lams_host[i];
+  for (int f = 0; f < nf; ++f) RP_REQUIRE(folds_host[f] >= -1, "rp_fold_systems: fold %d", folds_host[f]);
   cudaStream_t st = (cudaStream_t)stream;
-  if (A) {
-    if (nblocks <= 16)
-      fold_shift_kernel<16><<<d, 256, 0, st>>>(G, nblocks, d, s, nf, fa, A);
-    else
-      fold_shift_kernel<0><<<d, 256, 0, st>>>(G, nblocks, d, s, nf, fa, A);
-    RP_LAUNCH_CHECK("fold_shift");
-  }
-  if (rhs && m > 0) {
-    const int dp = ((d + 63) / 64) * 64;
-    fold_rhs_kernel<<<dim3(grid1d((int64_t)dp * m), nf), 256, 0, st>>>(C, nblocks, d, dp, m, fa, rhs);
-    RP_LAUNCH_CHECK("fold_rhs");
+  const int dp = ((d + 63) / 64) * 64;
+  // chunks of <= 64 folds x 32 lambdas per launch (kernel-parameter arrays); each element of the
+  // Gram blocks is read once per chunk
+  for (int f0 = 0; f0 < nf; f0 += FS_FOLDS) {
+    const int nfc = nf - f0 < FS_FOLDS ? nf - f0 : FS_FOLDS;
+    FoldSysArgs fa;
+    for (int f = 0; f < nfc; ++f) fa.folds[f] = folds_host[f0 + f];
+    if (A) {
+      for (int s0 = 0; s0 < s; s0 += FS_LAMS) {
+        const int sc = s - s0 < FS_LAMS ? s - s0 : FS_LAMS;
+        for (int i = 0; i < sc; ++i) fa.lams[i] = lams_host[s0 + i];
+        double* Ac = A + (int64_t)f0 * s * d * d;
+        if (nblocks <= 16)
+          fold_shift_kernel<16><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);
+        else
+          fold_shift_kernel<0><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);
+        RP_LAUNCH_CHECK("fold_shift");
+      }
+    }
+    if (rhs && m > 0) {
+      fold_rhs_kernel<<<dim3(grid1d((int64_t)dp * m), nfc), 256, 0, st>>>(C, nblocks, d, dp, m, fa,
+                                                                         rhs + (int64_t)f0 * dp * m);
+      RP_LAUNCH_CHECK("fold_rhs");
+    }
   }
   return RP_OK;
 }
@@ -959,50 +1017,67 @@ static int potrf_group(double* A, int d, int64_t stride, int batch, int* info, d
   return RP_OK;
 }
 
-size_t rp_fit_workspace_size(int d, int nf) { return sizeof(double) * (size_t)rp_tile_count(d) * nf; }
+// partials (ntiles x nf), then P and V for the general kernel
+size_t rp_fit_workspace_size(int d, int nf, int s, int r) {
+  if (d < 1 || nf < 1 || s < 1 || r < 0) return 0;
+  return sizeof(double) * ((size_t)rp_tile_count(d) * nf + 2 * (size_t)s * (r + 1));
+}
 
 int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_host, const double* V_host,
                  double* theta, double* resid, void* work, void* stream) {
-  RP_REQUIRE(d >= 1 && nf >= 1 && s >= 1 && s <= 32 && r >= 0 && r <= 4, "rp_fit_tiles: bad sizes");
-  FitArgs fa;
-  memset(&fa, 0, sizeof(fa));
-  for (int p = 0; p <= r; ++p)
-    for (int i = 0; i < s; ++i) {
-      fa.P[p][i] = P_host[p * s + i];
-      fa.V[i][p] = V_host[i * (r + 1) + p];
-    }
+  RP_REQUIRE(d >= 1 && nf >= 1 && s >= 1 && r >= 0 && s > r, "rp_fit_tiles: bad sizes d=%d nf=%d s=%d r=%d", d, nf,
+             s, r);
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nt = rp_tile_count(d);
-  if (s <= 8)
-    fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
-                                                                 (double*)work);
-  else
-    fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
-                                                                  (double*)work);
+  double* partial = (double*)work;
+  if (s <= 32 && r <= 4) {
+    FitArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    for (int p = 0; p <= r; ++p)
+      for (int i = 0; i < s; ++i) {
+        fa.P[p][i] = P_host[p * s + i];
+        fa.V[i][p] = V_host[i * (r + 1) + p];
+      }
+    if (s <= 8)
+      fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
+                                                                   partial);
+    else
+      fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
+                                                                    partial);
+  } else {
+    double* Pd = partial + (size_t)nt * nf;
+    double* Vd = Pd + (size_t)s * (r + 1);
+    const size_t pv = sizeof(double) * (size_t)s * (r + 1);
+    cudaError_t e = cudaMemcpyAsync(Pd, P_host, pv, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(Vd, V_host, pv, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "rp_fit_tiles: P / V upload");
+    fit_tiles_any_kernel<<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), Pd, Vd, theta,
+                                                                  partial);
+  }
   RP_LAUNCH_CHECK("fit_tiles");
   if (resid) {
-    fit_resid_kernel<<<nf, 256, 0, st>>>((double*)work, nt, resid);
+    fit_resid_kernel<<<nf, 256, 0, st>>>(partial, nt, resid);
     RP_LAUNCH_CHECK("fit_resid");
   }
   return RP_OK;
 }
 
 int rp_eval_materialize(const double* theta, int d, int r, double t, double* L, void* stream) {
-  RP_REQUIRE(d >= 1 && r >= 0 && r <= 4, "rp_eval_materialize: bad sizes");
+  RP_REQUIRE(d >= 1 && r >= 0, "rp_eval_materialize: bad sizes");
   materialize_kernel<<<grid1d((int64_t)d * d), 256, 0, (cudaStream_t)stream>>>(theta, d, r + 1, t, L);
   RP_LAUNCH_CHECK("materialize");
   return RP_OK;
 }
 
 int rp_theta_export(const double* theta, int d, int r, const int64_t* perm, int64_t D, double* out, void* stream) {
-  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0 && r <= 4, "rp_theta_export: bad sizes");
+  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0, "rp_theta_export: bad sizes");
   export_kernel<<<grid1d(D), 256, 0, (cudaStream_t)stream>>>(theta, d, r + 1, perm, D, out);
   RP_LAUNCH_CHECK("theta_export");
   return RP_OK;
 }
 
 int rp_theta_import(const double* vec, int d, int r, const int64_t* perm, int64_t D, double* theta, void* stream) {
-  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0 && r <= 4, "rp_theta_import: bad sizes");
+  RP_REQUIRE(d >= 1 && D >= 1 && r >= 0, "rp_theta_import: bad sizes");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = rp_theta_size(d, r);
   theta_init_kernel<<<grid1d(n), 256, 0, st>>>(theta, d, r + 1, rp_tile_count(d));

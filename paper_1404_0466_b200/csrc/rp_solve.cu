@@ -86,8 +86,40 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
   return pl;
 }
 
+// Degree > SOLVE_PMAX - 1 (not on the BASELINE path): each lambda's factor L(t_j) is evaluated into a
+// one-plane tile buffer (the same Horner arithmetic) and solved as a degree-0 "model".
+__global__ void theta_eval_kernel(const double* theta, int64_t fold_stride, int P, int64_t plane_elems,
+                                  const double* tval, double* out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // element of one plane set
+  const int f = blockIdx.y;
+  if (e >= plane_elems) return;
+  const int64_t tile = e / TILE_PLANE, w = e - tile * TILE_PLANE;
+  const double* th = theta + f * fold_stride + tile * P * TILE_PLANE + w;
+  const double t = *tval;
+  double v = th[(int64_t)(P - 1) * TILE_PLANE];
+  for (int p = P - 2; p >= 0; --p) v = fma(v, t, th[(int64_t)p * TILE_PLANE]);
+  out[(int64_t)f * plane_elems + e] = v;
+}
+
+__global__ void copy_cols_kernel(const double* src, int64_t lds, int64_t src_fold, double* dst, int64_t ldd,
+                                 int64_t dst_fold, int rows, int m) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int f = blockIdx.y;
+  if (e >= (int64_t)rows * m) return;
+  const int64_t i = e / m;
+  const int o = (int)(e - i * m);
+  dst[f * dst_fold + i * ldd + o] = src[f * src_fold + i * lds + o];
+}
+
+static int eval_solve_planned(const double* theta, int d, int r, int nf, const double* rhs, int m, const double* tvals,
+                              int q, double* W, int64_t ldw, int* flags, int flag_stride, void* work,
+                              cudaStream_t st);
+
 extern "C" size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int q) {
-  if (d < 1 || nf < 1 || m < 1 || m > 16 || q < 1 || r < 0 || r + 1 > SOLVE_PMAX) return 0;
+  if (d < 1 || nf < 1 || m < 1 || m > 16 || q < 1 || r < 0) return 0;
+  if (r + 1 > SOLVE_PMAX)  // one-plane tiles + a column block of solutions + the degree-0 solve's rows
+    return sizeof(double) * (size_t)nf * (rp_theta_size(d, 0) + (size_t)((d + 63) / 64 * 64) * (m + (m & 1))) +
+           rp_eval_solve_workspace_size(d, 0, nf, m, 1);
   const SolvePlan pl = plan_solve(d, r, nf, m, q);
   if (pl.lam == 0) return 0;
   return sizeof(double) * (size_t)nf * pl.chunks * (size_t)pl.nt * 64 * pl.S;
@@ -97,13 +129,39 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
                              const double* tvals, int q, double* W, int64_t ldw, int* flags, void* work,
                              void* stream) {
   RP_REQUIRE(d >= 1 && nf >= 1 && q >= 1, "rp_eval_solve: bad sizes d=%d nf=%d q=%d", d, nf, q);
-  RP_REQUIRE(r >= 0 && r + 1 <= SOLVE_PMAX, "rp_eval_solve: degree %d outside [0, %d]", r, SOLVE_PMAX - 1);
+  RP_REQUIRE(r >= 0, "rp_eval_solve: degree %d", r);
   RP_REQUIRE(m >= 1 && m <= 16, "rp_eval_solve: %d outputs per call (max 16)", m);
   RP_REQUIRE(ldw >= (int64_t)q * m && ldw % 2 == 0, "rp_eval_solve: ldw=%lld must be even and >= q*m",
              (long long)ldw);
   RP_REQUIRE(((uintptr_t)theta & 15) == 0 && ((uintptr_t)W & 15) == 0, "rp_eval_solve: 16-byte alignment");
   RP_REQUIRE(work != nullptr && ((uintptr_t)work & 15) == 0, "rp_eval_solve: workspace (16-byte aligned)");
   cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
+  if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");
+  if (r + 1 <= SOLVE_PMAX) return eval_solve_planned(theta, d, r, nf, rhs, m, tvals, q, W, ldw, flags, q, work, st);
+  // high degree: per lambda, L(t_j) into a one-plane tile buffer, then a degree-0 solve of that column block
+  const int dp = (d + 63) / 64 * 64, mp = m + (m & 1);
+  double* th0 = (double*)work;
+  const int64_t plane = rp_theta_size(d, 0);
+  double* wcol = th0 + (size_t)nf * plane;  // nf x dp x mp
+  void* work2 = wcol + (size_t)nf * dp * mp;
+  for (int j = 0; j < q; ++j) {
+    theta_eval_kernel<<<dim3((unsigned)((plane + 255) / 256), nf), 256, 0, st>>>(theta, rp_theta_size(d, r), r + 1,
+                                                                                 plane, tvals + j, th0);
+    RP_LAUNCH_CHECK("theta_eval");
+    int rc = eval_solve_planned(th0, d, 0, nf, rhs, m, tvals + j, 1, wcol, mp, flags + j, q, work2, st);
+    if (rc) return rc;
+    copy_cols_kernel<<<dim3((unsigned)(((int64_t)dp * m + 255) / 256), nf), 256, 0, st>>>(
+        wcol, mp, (int64_t)dp * mp, W + (int64_t)j * m, ldw, (int64_t)dp * ldw, dp, m);
+    RP_LAUNCH_CHECK("solve column copy");
+  }
+  return RP_OK;
+}
+
+static int eval_solve_planned(const double* theta, int d, int r, int nf, const double* rhs, int m, const double* tvals,
+                              int q, double* W, int64_t ldw, int* flags, int flag_stride, void* work,
+                              cudaStream_t st) {
+  RP_REQUIRE(((uintptr_t)W & 15) == 0, "rp_eval_solve: 16-byte alignment of the W column block");
   const SolvePlan pl = plan_solve(d, r, nf, m, q);
   RP_REQUIRE(pl.lam >= 1, "rp_eval_solve: no chunk size fits shared memory");
   const int P = pl.P, nt = pl.nt;
@@ -133,6 +191,7 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   a.w_fold_stride = (int64_t)nt * 64 * ldw;
   a.tvals = tvals;
   a.flags = flags;
+  a.flag_stride = flag_stride;
   a.q = q;
   a.m = m;
   a.d = d;
@@ -143,8 +202,6 @@ extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const do
   a.S = pl.S;
   a.Wc = (double*)work;
   const int grid = nf * a.chunks;
-  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)nf * q, st);
-  if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve memset");
   if (pl.fast) return launch_solve_fast(m, P, pl.lam, a, grid, st);
   return launch_generic(m, a, grid, st);
 }

@@ -61,6 +61,7 @@ struct SolveArgs {
   int64_t ldw, w_fold_stride;
   const double* tvals;
   int* flags;
+  int flag_stride;  // flags of fold f at flags + f * flag_stride (q unless a caller splits the grid)
   int q, m, d, nt, P, lam_per_cta, chunks, S;
   double* Wc;      // chunk-private rows of the solution (dp x S per CTA)
   int64_t ntiles;  // 64 x 64 tiles per fold
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
         sLev[(l * 16 + i) * 17 + j] = v;
         if (i == j) {
           sRinv[l * 16 + i] = __drcp_rn(v);  // = 1.0 / v (correctly rounded), without the division path
-          if (!BWD && rowI + r0 + i < a.d && !(fabs(v) >= 1e-12)) a.flags[fold * a.q + l0 + l] = 1;
+          if (!BWD && rowI + r0 + i < a.d && !(fabs(v) >= 1e-12)) a.flags[fold * a.flag_stride + l0 + l] = 1;
         }
       }
       __syncthreads();

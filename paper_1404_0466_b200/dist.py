@@ -13,7 +13,9 @@ exchanges are real data dependencies of the path:
   c4) and every rank runs the same ordered fold mean + argmin.
 
 The hooks operate on torch tensors only, so the same code runs on CPU tensors
-with the gloo backend (tests/test_dist_gloo.py).
+with the gloo backend (tests/test_dist_gloo.py), and on CUDA tensors over gloo
+by staging through host memory (two ranks sharing one GPU in
+tests/test_gpu_dist.py; NCCL is the backend on a multi-GPU node).
 """
 
 from __future__ import annotations
@@ -37,9 +39,10 @@ class Shard:
 
     @property
     def gram_blocks(self):
-        """Blocks whose Gram this rank computes."""
+        """Blocks whose Gram this rank computes (none for a rank without folds when the blocks
+        are replicated: world > k leaves ranks k..world-1 with only the curve exchange)."""
         if not self.exchange:
-            return list(range(self.k))
+            return list(range(self.k)) if self.local_folds else []
         per = self.k // self.world
         return list(range(self.rank * per, (self.rank + 1) * per))
 
@@ -53,23 +56,39 @@ class Shard:
         return f if f < self.k else None
 
 
-def exchange_grams(shard, G, C, yy=None, group=None):
-    """All-gather contiguous Gram blocks so every rank holds all k (G: (k, d, d), C: (k, m, d))."""
+def _host_staged(t, group=None):
+    """True when the process group cannot run collectives on ``t``'s device (gloo with CUDA
+    tensors: the exchange is staged through pinned host memory instead)."""
     import torch.distributed as dist
 
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def _all_gather_into(out, mine, group=None):
+    import torch.distributed as dist
+
+    if _host_staged(out, group):
+        host = out.new_empty(out.shape, device="cpu")
+        dist.all_gather_into_tensor(host, mine.cpu(), group=group)
+        out.copy_(host)
+    else:
+        dist.all_gather_into_tensor(out, mine, group=group)
+
+
+def exchange_grams(shard, G, C, yy=None, group=None):
+    """All-gather contiguous Gram blocks so every rank holds all k (G: (k, d, d), C: (k, m, d))."""
     if not shard.exchange:
         return
     per = shard.k // shard.world
     lo = shard.rank * per
     for buf in (G, C) + ((yy,) if yy is not None else ()):
         mine = buf[lo : lo + per].clone()
-        dist.all_gather_into_tensor(buf, mine, group=group)
+        _all_gather_into(buf, mine, group=group)
 
 
 def gather_curves(shard, curves_local, group=None):
     """All-gather per-fold curves (nf_local, q, m) into fold order (k, q, m)."""
     import torch
-    import torch.distributed as dist
 
     if shard.world == 1:
         return curves_local
@@ -78,7 +97,7 @@ def gather_curves(shard, curves_local, group=None):
     pad = torch.zeros((slots, q, m), dtype=curves_local.dtype, device=curves_local.device)
     pad[:nf].copy_(curves_local)
     out = torch.empty((shard.world * slots, q, m), dtype=curves_local.dtype, device=curves_local.device)
-    dist.all_gather_into_tensor(out, pad, group=group)
+    _all_gather_into(out, pad, group=group)
     order = []
     for f in range(shard.k):
         order.append((f % shard.world) * slots + f // shard.world)

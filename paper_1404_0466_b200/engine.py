@@ -91,6 +91,13 @@ class PicholEngine:
         torch, dev = self.torch, self.device
         f64 = dict(dtype=torch.float64, device=dev)
         d, dp, k, nf, s, q, m = self.d, self.dp, self.k, self.nf, self.s, self.q, self.m
+        if nf == 0:  # a rank without folds (world > k): it only joins the curve exchange
+            self.curves = torch.empty((0, q, m), **f64)
+            self.mean = torch.empty((q, m), **f64)
+            self.best = torch.empty((m,), dtype=torch.int32, device=dev)
+            self.info = torch.zeros((0,), dtype=torch.int32, device=dev)
+            self.flags = torch.zeros((len(self.groups), 0, q), dtype=torch.int32, device=dev)
+            return
         self.G = torch.empty((k, d, d), **f64)
         self.C = torch.empty((k, m, d), **f64)  # C_b column-major d x m == (m, d) row-major
         self.yy = torch.empty((k, m), **f64)
@@ -119,7 +126,7 @@ class PicholEngine:
         self.ws_gram = torch.empty((max(_lib.query("rp_gram_workspace_size", d, self.block_rows[0], ng),
                                         _lib.query("rp_gram_workspace_size", d, max(self.block_rows), 1)),), **u8)
         self.ws_potrf = torch.empty((_lib.query("rp_potrf_workspace_size", d, nf * s),), **u8)
-        self.ws_fit = torch.empty((_lib.query("rp_fit_workspace_size", d, nf),), **u8)
+        self.ws_fit = torch.empty((_lib.query("rp_fit_workspace_size", d, nf, s, self.r),), **u8)
         nval = max(self.block_rows[f] for f in self.local_folds)
         mg = max(c1 - c0 for c0, c1 in self.groups)
         self.ws_hold = torch.empty((_lib.query("rp_holdout_workspace_size", nval, d, q, mg, 1 if not self.equal_blocks else nf),), **u8)
@@ -265,6 +272,12 @@ class PicholEngine:
                 ev.append((name, e))
 
         mark("start")
+        if self.nf == 0:
+            curves_all = gather_curves(self.curves) if gather_curves is not None else self.curves
+            if curves_all.shape[0] == self.k:
+                self.stage_select(curves_all)
+                return curves_all, self.mean, self.best
+            return curves_all, None, None
         self.stage_gram(X, Y, block_ready)
         if block_ready is not None:  # later stages may read any row of X / Y
             for done in block_ready.values():

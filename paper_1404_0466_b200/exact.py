@@ -97,7 +97,7 @@ class ExactEvaluator:
         resid = _dev.empty((nmod,))
         one = np.ones((1, 1))
         call("rp_fit_tiles", ptr(A), d, 1, nmod, 0, _lib.host_ptr(one), _lib.host_ptr(one), ptr(theta), ptr(resid),
-             ptr(_dev.workspace(_lib.query("rp_fit_workspace_size", d, nmod))), st)
+             ptr(_dev.workspace(_lib.query("rp_fit_workspace_size", d, nmod, 1, 0))), st)
         del A
         zero_t = _dev.zeros((1,))
         out = np.empty((nf, nb, m))

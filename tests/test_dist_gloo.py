@@ -84,6 +84,10 @@ def test_shard_placement():
     assert s.local_folds == [1] and not s.exchange and s.gram_blocks == list(range(5))
     s = Shard(1, 2, 8)
     assert s.local_folds == [1, 3, 5, 7] and s.exchange and s.gram_blocks == [4, 5, 6, 7]
+    # world > k (c1-c3 have k = 5 on an 8-GPU node): ranks without folds compute nothing and only
+    # join the curve exchange
+    s = Shard(6, 8, 5)
+    assert s.local_folds == [] and not s.exchange and s.gram_blocks == [] and s.slots == 1
 
 
 def test_two_rank_gloo_matches_single_process():

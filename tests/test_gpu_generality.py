@@ -1,0 +1,56 @@
+"""Shapes the reference accepts beyond the BASELINE configs (pichol.py:92-103: any g > r;
+cvsearch.py:76-92: any k <= n): high polynomial degree (the solve evaluates each lambda's factor
+into a one-plane tile buffer when degree > 4), more than 32 sampled lambdas (P and V leave the
+kernel parameters), more than 64 folds (the shifted systems are assembled in chunks), odd output
+counts and non-multiple-of-64 dimensions -- all against the CPU oracle."""
+
+import numpy as np
+import pytest
+
+from oracle import pichol_oracle as orc
+from paper_1404_0466_b200 import _dev, configs, cvsearch, pichol
+from paper_1404_0466_b200.engine import PicholEngine
+from tests.helpers import rel
+
+pytestmark = pytest.mark.gpu
+
+
+def sweep_vs_oracle(n, d, m, k, q, s, r, lo=1e-2, hi=1e1, seed=0):
+    X, Y = configs.powerlaw(n, d, m, seed=seed)
+    grid = orc.make_grid(lo, hi, q)
+    lams, V, _, ts, tsh, P = pichol.fit_basis(grid[orc.sample_indices(q, s)], r)
+    eng = PicholEngine([n // k] * k, d, m, q, s, r)
+    curves, mean, best = eng.sweep(_dev.to_dev(X), _dev.to_dev(Y), lams, P, V, ts * grid + tsh)
+    assert eng.check_numerics(lams) is None
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(n, k), k, grid, g=s, r=r)
+    return curves.cpu().numpy(), best.cpu().numpy(), ref
+
+
+@pytest.mark.parametrize("r,s,m", [(5, 8, 3), (7, 9, 1)])
+def test_high_degree_matches_oracle(gpu, r, s, m):
+    curves, best, ref = sweep_vs_oracle(1200, 70, m, 4, 11, s, r)
+    assert rel(curves, ref["curves"]) <= 1e-8
+    assert np.array_equal(best, ref["best"])
+
+
+def test_many_sampled_lambdas_matches_oracle(gpu):
+    curves, best, ref = sweep_vs_oracle(1500, 48, 2, 3, 45, 40, 2)
+    assert rel(curves, ref["curves"]) <= 1e-8
+    assert np.array_equal(best, ref["best"])
+
+
+def test_more_than_64_folds_matches_oracle(gpu):
+    curves, best, ref = sweep_vs_oracle(70 * 40, 12, 2, 70, 7, 4, 2)
+    assert rel(curves, ref["curves"]) <= 1e-8
+    assert np.array_equal(best, ref["best"])
+
+
+def test_drop_in_high_degree_report(gpu):
+    """Through the drop-in driver (cvsearch.grid_search_pichol) with g = 7, r = 5."""
+    X, Y = configs.powerlaw(900, 40, 1, seed=8)
+    grid = cvsearch.make_grid(1e-2, 1e1, 13)
+    rep = cvsearch.grid_search_pichol(cvsearch.Dataset(X, Y[:, 0]), grid, cvsearch.contiguous_folds(900, 3),
+                                      g=7, r=5)
+    ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(900, 3), 3, grid.values, g=7, r=5)
+    assert rel(rep.curves, ref["curves"]) <= 1e-8
+    assert rep.best_lambda == float(grid.values[int(ref["best"][0])])
