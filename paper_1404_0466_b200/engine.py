@@ -97,6 +97,7 @@ class PicholEngine:
             self.best = torch.empty((m,), dtype=torch.int32, device=dev)
             self.info = torch.zeros((0,), dtype=torch.int32, device=dev)
             self.flags = torch.zeros((len(self.groups), 0, q), dtype=torch.int32, device=dev)
+            self.tvals = torch.empty((q,), **f64)
             return
         self.G = torch.empty((k, d, d), **f64)
         self.C = torch.empty((k, m, d), **f64)  # C_b column-major d x m == (m, d) row-major
