@@ -11,12 +11,19 @@ e2e = the same metric through the public API (cvsearch.CvSession.run) with
 pinned host X/Y copied in and curves + selection read back every step.
 
 Under torchrun (N > 1) folds are sharded f -> rank f % N; Gram blocks and
-curves are all-gathered over NCCL (paper_1404_0466_b200/dist.py).
+curves are all-gathered over NCCL (paper_1404_0466_b200/dist.py). The c4
+problem is fixed as N grows, so "scaling" is "strong".
+
+Also reported: fp64_only (the same sweep with every product on FP64 DMMA, no
+int8 Ozaki emulation), dropin (the literal cvsearch.grid_search_pichol call on
+numpy arrays), the dominant kernel's roofline, per-stage times.
 
 --impl reference times the CPU oracle port (oracle/pichol_oracle.py, a line-by-
-line restatement of the reference package, which is pure Python) on the host
-cores, on a bounded sample of the same workload (one fold's setup + a few
-lambdas per step, extrapolated to the full sweep).
+line restatement of the reference package, which is pure Python and cannot
+travel to the GPU box) on the host cores in the reference's fastest mode there
+(its fold thread pool, threads=k, one BLAS thread per fold), on a bounded
+sample of the same workload (every fold's setup + a few lambdas per step,
+extrapolated to the full sweep). tools/cpu_modes.py measures the other modes.
 """
 
 from __future__ import annotations
@@ -48,8 +55,10 @@ def parse():
     ap.add_argument("--holdout", default="auto", choices=["auto", "gram", "direct"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-lams", type=int, default=4, help="lambdas timed per CPU sample")
+    ap.add_argument("--cpu-lams", type=int, default=2, help="lambdas timed per fold per CPU sample")
     ap.add_argument("--profile-stages", action="store_true", help="print per-stage timings to stderr")
+    ap.add_argument("--no-fp64-only", action="store_true", help="skip the all-FP64 (no Ozaki) sweep timing")
+    ap.add_argument("--no-dropin", action="store_true", help="skip timing cvsearch.grid_search_pichol")
     return ap.parse_args()
 
 
@@ -61,25 +70,35 @@ def dist_env():
 
 
 def peaks():
-    """Roofline denominators: driver-measured HBM copy; FP64 DMMA measured by tools/fp64_peaks.cu."""
-    out = {"hbm_gbs": 6552.0, "hbm_src": "fallback", "fp64_tflops": 37.0, "fp64_src": "fallback"}
+    """Roofline denominators and where each comes from.
+
+    HBM: the driver-measured copy bandwidth (MEASURED_PEAKS.json). FP64: there is no driver-measured FP64
+    figure, so the builder-measured mma.sync.m8n8k4.f64 rate on this pool's B200 (tools/fp64_peaks.cu ->
+    profiles/r01_fp64_peaks.json, best of the runs; the B200_PROFILING fallback has no FP64 entry). int8:
+    the best builder-measured tcgen05.mma kind::i8 rate (tools/ozaki_test.cu peak mode ->
+    profiles/r01_int8_peak.json; M=128 N=256 beats the N=128 shape the kernels issue, so the denominator
+    is the larger, stricter one)."""
+    out = {"hbm_gbs": 6552.0, "hbm_src": "fallback", "fp64_tflops": 37.0, "fp64_src": "fallback",
+           "i8_tops": 4500.0, "i8_src": "fallback (nominal dense int8)"}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
             out["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
-            out["hbm_src"] = "MEASURED_PEAKS.json"
+            out["hbm_src"] = "MEASURED_PEAKS.json (driver-measured copy)"
     p = os.path.join(ROOT, "profiles", "r01_fp64_peaks.json")
     if os.path.exists(p):
         with open(p) as f:
             vals = [json.loads(line) for line in f if line.strip()]
-        out["fp64_tflops"] = max(v["dmma884_tflops_b4"] for v in vals)
-        out["fp64_src"] = "profiles/r01_fp64_peaks.json (mma.sync.m8n8k4.f64, burst)"
-    out["i8_tops"], out["i8_src"] = 4500.0, "fallback (nominal dense int8)"
+        out["fp64_tflops"] = max(max(v["dmma884_tflops_b4"], v.get("dmma16816_tflops_b2", 0.0)) for v in vals)
+        out["fp64_src"] = ("builder-measured: profiles/r01_fp64_peaks.json (tools/fp64_peaks.cu, mma.sync f64 "
+                           "back to back on 148 SMs, best shape and run; no driver-measured FP64 peak exists)")
     p = os.path.join(ROOT, "profiles", "r01_int8_peak.json")
     if os.path.exists(p):
         with open(p) as f:
-            out["i8_tops"] = float(json.load(f)["i8_tops_n128"])
-        out["i8_src"] = "profiles/r01_int8_peak.json (tcgen05.mma kind::i8 M=128 N=128, burst)"
+            j = json.load(f)
+        out["i8_tops"] = max(float(v) for kk, v in j.items() if kk.startswith("i8_tops_"))
+        out["i8_src"] = ("builder-measured: profiles/r01_int8_peak.json (tools/ozaki_test.cu, tcgen05.mma "
+                         "kind::i8 back to back from shared memory, best shape M=128 N=256)")
     return out
 
 
@@ -105,17 +124,49 @@ def ozaki_holdout_ops(cfg, nf, mg):
     return nf * nt * ksteps * OZ_PAIRS * 2.0 * 128 * 128 * 32
 
 
-def ncu_traffic(stage):
-    """DRAM bytes (read + write) per launch of a stage's main kernel from the committed
-    `ncu --set full` capture (profiles/r01_ncu_top_kernels.json), else None."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_top_kernels.json")
-    key = {"gram": "gram_syrk", "oz_syrk": "oz_syrk", "eval_solve": "eval_solve",
-           "holdout_gemm": "holdout_gemm", "oz_holdout": "oz_holdout"}.get(stage)
+def ncu_traffic(stage, config):
+    """DRAM bytes (read + write) per launch of a stage's main kernel, for this config, from the committed
+    `ncu --set full` captures (profiles/r02_ncu_top_kernels.json: {config: {kernel: {...}}}), else None."""
+    p = os.path.join(ROOT, "profiles", "r02_ncu_top_kernels.json")
+    key = {"oz_syrk": "oz_syrk", "eval_solve": "eval_solve", "holdout_gemm": "holdout_gemm",
+           "oz_holdout": "oz_holdout"}.get(stage)
     if key is None or not os.path.exists(p):
         return None
     with open(p) as f:
-        k = json.load(f).get(key)
+        k = json.load(f).get(config, {}).get(key)
     return None if k is None else k["dram_read_bytes"] + k["dram_write_bytes"]
+
+
+def host_info():
+    """CPU model, core count and BLAS build of the host that ran the CPU baseline."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), None)
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = sorted({f"{i.get('internal_api')} {i.get('version')}" for i in threadpool_info()})
+    except Exception:  # noqa: BLE001 -- informational only
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "numpy": np.__version__, "blas": blas}
+
+
+def cpu_modes(config):
+    """The other CPU modes of SURVEY 8(d) (stock driver per output; threads=k with 1-thread BLAS), measured
+    once per round on the GPU box's host by tools/cpu_modes.py (too long for every bench run)."""
+    for tag in ("r02", "r01"):
+        p = os.path.join(ROOT, "profiles", f"{tag}_cpu_modes_{config}.json")
+        if os.path.exists(p):
+            with open(p) as f:
+                j = json.load(f)
+            return {"source": f"profiles/{tag}_cpu_modes_{config}.json (tools/cpu_modes.py)", "host": j["host"],
+                    **{k: {"value": v["value"], "cores": v["cores"], "sample": v["sample"]}
+                       for k, v in j["modes"].items()}}
+    return None
 
 
 class ClockSampler:
@@ -205,24 +256,51 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def cpu_fold_threads(cfg, X, Y, n_lam):
+    """The reference's fastest CPU mode on this host: its fold thread pool (threads=k, cvsearch.py:126-142,
+    cli.py:322) with one BLAS thread per fold, each fold doing the multi-RHS work (setup + n_lam lambdas for
+    all m outputs). tools/cpu_modes.py measured the alternatives on the GPU box (profiles/r02_cpu_modes_c4.json:
+    all-threads BLAS with sequential folds 1.7 evals/s, the stock single-target driver per output 0.18, this
+    mode 8.5). Returns (evals/s extrapolated to the k x q sweep, threads used, details)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+
+    cores = cpu_cores()
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=min(cfg.k, cores)) as pool:
+            res = list(pool.map(lambda f: cpu_sample(cfg, X, Y, f, n_lam), range(cfg.k)))
+        wall = time.perf_counter() - t0
+    setup = max(r[0] for r in res)
+    lam = max(r[1] for r in res)
+    waves = -(-cfg.k // cores)
+    value = cfg.k * cfg.q / (waves * (setup + cfg.q * lam))
+    return value, min(cfg.k, cores), {"t_setup_s_max": setup, "t_lambda_s_max": lam, "sample_wall_s": wall}
+
+
+def fold_thread_sample_text(cfg, n_lam):
+    return (f"{cfg.name}: all k={cfg.k} folds concurrently on the reference's fold thread pool, 1 BLAS thread "
+            f"each; per fold assemble + {cfg.s} Choleskys + fit + {n_lam} of {cfg.q} lambdas (m={cfg.m} RHS) on the "
+            f"oracle port, extrapolated linearly to all {cfg.q} lambdas")
+
+
 def run_reference(args, cfg, world, rank):
     if rank != 0:
         return
     from paper_1404_0466_b200 import configs
 
     X, Y = configs.generate(cfg)
-    step_times, setups, lams = [], [], []
-    for i in range(args.warmup + args.steps):
-        fold = i % cfg.k
-        t_setup, t_lam = cpu_sample(cfg, X, Y, fold, args.cpu_lams)
-        if i >= args.warmup:
-            setups.append(t_setup)
-            lams.append(t_lam)
-            step_times.append(t_setup + cfg.q * t_lam)  # one fold's full lambda sweep, extrapolated
-    per_fold = float(np.mean(step_times))
-    value = cfg.q / per_fold  # k*q evals / (k * per-fold time)
-    sample = (f"per step: fold i%k of {cfg.name} (assemble + {cfg.s} Choleskys + fit) + {args.cpu_lams} of "
-              f"{cfg.q} lambdas, extrapolated linearly to all {cfg.q} lambdas and k={cfg.k} folds")
+    warm = configs.CONFIGS["c1"]
+    Xw, Yw = configs.generate(warm)
+    for _ in range(args.warmup):  # page in BLAS, scipy and the thread pool on a small problem
+        cpu_fold_threads(warm, Xw, Yw, 1)
+    vals, details, cores = [], [], 1
+    for _ in range(args.steps):
+        v, cores, det = cpu_fold_threads(cfg, X, Y, args.cpu_lams)
+        vals.append(v)
+        details.append(det)
+    value = float(np.mean(vals))
     out = {
         "impl": "reference",
         "metric": METRIC,
@@ -231,15 +309,16 @@ def run_reference(args, cfg, world, rank):
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": per_fold * cfg.k * 1e3,
+        "ms_per_step": cfg.k * cfg.q / value * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator, paper_1404_0466_b200/configs.py)",
         "config": config_dict(cfg, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "port", "sample": sample,
-                         "t_setup_s": float(np.mean(setups)), "t_lambda_s": float(np.mean(lams))},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": fold_thread_sample_text(cfg, args.cpu_lams), "steps": details,
+                         "host": host_info(), "modes": cpu_modes(cfg.name)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
@@ -340,6 +419,34 @@ def run_ours(args, cfg, world, rank, local):
     kern_ms["eval_solve"] = sum(solve_split)
     _lib.call("rp_set_option", b"profile", 0)
 
+    # ---- the all-FP64 path (every product on FP64 DMMA, no int8 Ozaki emulation), same data, same timing
+    fp64_only = None
+    if not args.no_fp64_only:
+        opts = {b"gram_dmma": (1, 0), b"chol_ozaki": (0, 1), b"holdout_ozaki": (0, 1)}
+        for o, (v, _) in opts.items():
+            _lib.call("rp_set_option", o, v)
+        sess.sweep()
+        n64 = max(2, min(args.steps, 3))
+        barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(n64):
+            sess.sweep()
+        f1.record()
+        torch.cuda.synchronize()
+        ms64 = f0.elapsed_time(f1) / n64
+        if world > 1:
+            t = torch.tensor([ms64], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms64 = float(t.item())
+        for o, (_, v) in opts.items():
+            _lib.call("rp_set_option", o, v)
+        fp64_only = {"value": cfg.k * cfg.q / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64, "steps": n64,
+                     "options": "gram_dmma=1 chol_ozaki=0 holdout_ozaki=0 (Gram, Cholesky trailing updates and "
+                                "hold-out on FP64 DMMA instead of the int8 Ozaki scheme)"}
+
     # ---- end to end through the public API (pinned host in, curves + argmin out)
     e2e_steps = max(1, args.e2e_steps) if args.e2e_steps is not None else max(2, min(args.steps, 3))
     sess.run(Xp, Yp)
@@ -353,6 +460,28 @@ def run_ours(args, cfg, world, rank, local):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         t_e2e = float(t.item())
     e2e_value = cfg.k * cfg.q / t_e2e
+
+    # ---- the literal drop-in call (cvsearch.grid_search_pichol on numpy arrays, single GPU): the first call
+    # builds the shape-keyed session (device buffers), later calls reuse it
+    dropin = None
+    if world == 1 and not args.no_dropin:
+        from paper_1404_0466_b200 import cvsearch as cvs
+
+        ds = cvs.Dataset(X, Y)
+        grid_obj = cvs.make_grid(cfg.lo, cfg.hi, cfg.q)
+        folds = cvs.contiguous_folds(cfg.n, cfg.k)
+        t0 = time.perf_counter()
+        rep = cvs.grid_search_pichol(ds, grid_obj, folds, g=cfg.s, r=cfg.r)
+        t_first = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        rep = cvs.grid_search_pichol(ds, grid_obj, folds, g=cfg.s, r=cfg.r)
+        t_call = time.perf_counter() - t0
+        same = bool(np.array_equal(rep.best_index, best))
+        cvs.clear_session_cache()
+        dropin = {"value": cfg.k * cfg.q / t_call, "unit": UNIT, "call_s": t_call, "first_call_s": t_first,
+                  "h2d_bytes_per_call": (X.size + Y.size) * 8, "same_selection_as_session": same,
+                  "note": "cvsearch.grid_search_pichol(Dataset(X, Y), ...) with pageable numpy X/Y, report built "
+                          "on the host; the first call allocates the cached session"}
 
     # ---- roofline of the dominant stage
     pk = peaks()
@@ -396,7 +525,7 @@ def run_ours(args, cfg, world, rank, local):
         kv = kernels[dom]
         per = kv["launches"]
         roof = {"bound": "tensor", "kernel": dom, "achieved": kv["achieved"], "peak": kv["peak"], "unit": kv["unit"],
-                "frac": kv["frac"], "traffic": ncu_traffic(dom), "peak_src": kv["peak_src"],
+                "frac": kv["frac"], "traffic": ncu_traffic(dom, cfg.name), "peak_src": kv["peak_src"],
                 "work_per_launch": kv["work"] / per, "ms_per_launch": kv["ms"] / per}
         if "fp64_equivalent_tflops" in kv:
             roof["fp64_equivalent_tflops"] = kv["fp64_equivalent_tflops"]
@@ -415,7 +544,7 @@ def run_ours(args, cfg, world, rank, local):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded generator, paper_1404_0466_b200/configs.py)",
@@ -424,18 +553,17 @@ def run_ours(args, cfg, world, rank, local):
                 "d2h_bytes_per_step": sess.d2h_bytes, "ms_per_step": t_e2e * 1e3},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        "fp64_only": fp64_only,
+        "dropin": dropin,
         "roofline": roof,
         "kernels": kernels,
         "stages": stages,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        t_setup, t_lam = cpu_sample(cfg, X, Y, 0, args.cpu_lams)
-        cpu_val = cfg.q / (t_setup + cfg.q * t_lam)
-        out["cpu_baseline"] = {
-            "value": cpu_val, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
-            "sample": f"fold 0 of {cfg.name}: assemble + {cfg.s} Choleskys + fit + {args.cpu_lams} of {cfg.q} "
-                      f"lambdas on the oracle port, extrapolated to the full sweep",
-            "t_setup_s": t_setup, "t_lambda_s": t_lam}
+        cpu_val, cores, det = cpu_fold_threads(cfg, X, Y, 1)
+        out["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
+                               "sample": fold_thread_sample_text(cfg, 1), **det, "host": host_info(),
+                               "modes": cpu_modes(cfg.name)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -305,6 +305,35 @@ class CvSession:
         return curves.cpu().numpy(), best.cpu().numpy()
 
 
+_SESSION_CACHE = {}  # shape key -> CvSession (the most recent shape only)
+
+
+def _cached_session(counts, d, m, grid_values, g, r, metric, holdout, raw_monomials):
+    """A CvSession for these shapes and this grid, reused across drop-in calls.
+
+    A session preallocates every device buffer of the sweep (about 18 GB at c4), so repeated
+    grid_search_pichol calls on the same shapes -- the reference's usage pattern: one call per
+    target or per dataset of a fixed design -- allocate once. Only the most recent shape is kept,
+    so switching shapes releases the previous buffers."""
+    import torch
+
+    key = (tuple(int(c) for c in counts), int(d), int(m), np.asarray(grid_values, dtype=float).tobytes(), int(g),
+           int(r), metric, holdout, bool(raw_monomials),
+           torch.cuda.current_device() if torch.cuda.is_available() else -1)
+    sess = _SESSION_CACHE.get(key)
+    if sess is None:
+        _SESSION_CACHE.clear()
+        sess = CvSession(counts, d, m, grid_values, g=g, r=r, metric=metric, holdout=holdout,
+                         raw_monomials=raw_monomials)
+        _SESSION_CACHE[key] = sess
+    return sess
+
+
+def clear_session_cache():
+    """Release the device buffers held for repeated grid_search_pichol calls."""
+    _SESSION_CACHE.clear()
+
+
 def grid_search_pichol(
     p,
     grid,
@@ -336,8 +365,7 @@ def grid_search_pichol(
         raise InvalidThreshold(f"recursion threshold must be >= 1, got {h0}")
     X, Y, counts = prepare_design(p, folds)
     n, d = X.shape
-    sess = CvSession(counts, d, Y.shape[1], grid.values, g=g, r=r, metric=metric, holdout=holdout,
-                     raw_monomials=raw_monomials)
+    sess = _cached_session(counts, d, Y.shape[1], grid.values, g, r, metric, holdout, raw_monomials)
     timings = {}
     curves, _ = sess.run(X, Y, timings=timings)
     k = folds.k

@@ -37,6 +37,30 @@ def test_c1_matches_reference_golden(gpu, holdout):
     assert len(cvsearch.report_csv_lines(rep)) == 1 + c1.k * c1.q + c1.q
 
 
+def test_dropin_reuses_its_session_per_shape(gpu):
+    """Repeated grid_search_pichol calls on one shape reuse one device session (no reallocation) and
+    give identical reports; a new shape replaces the cached session."""
+    c1 = configs.CONFIGS["c1"]
+    X, Y = configs.generate(c1)
+    grid = cvsearch.make_grid(c1.lo, c1.hi, c1.q)
+    folds = cvsearch.contiguous_folds(c1.n, c1.k)
+    cvsearch.clear_session_cache()
+    r1 = cvsearch.grid_search_pichol(cvsearch.Dataset(X, Y[:, 0]), grid, folds, g=c1.s, r=c1.r)
+    sess = list(cvsearch._SESSION_CACHE.values())
+    r2 = cvsearch.grid_search_pichol(cvsearch.Dataset(X, Y[:, 0]), grid, folds, g=c1.s, r=c1.r)
+    assert list(cvsearch._SESSION_CACHE.values()) == sess and len(sess) == 1
+    assert np.array_equal(r1.curves, r2.curves) and r1.best_lambda == r2.best_lambda
+    # a different target on the same design: same shapes, same session, its own curves
+    r3 = cvsearch.grid_search_pichol(cvsearch.Dataset(X, -Y[:, 0] + 1.0), grid, folds, g=c1.s, r=c1.r)
+    assert list(cvsearch._SESSION_CACHE.values()) == sess
+    ref = orc.grid_search_pichol(X, (-Y[:, 0] + 1.0)[:, None], folds.assignments, c1.k, grid.values, g=c1.s, r=c1.r)
+    assert rel(r3.curves, ref["curves"]) <= 1e-8
+    grid2 = cvsearch.make_grid(c1.lo, c1.hi, c1.q + 1)
+    cvsearch.grid_search_pichol(cvsearch.Dataset(X, Y[:, 0]), grid2, folds, g=c1.s, r=c1.r)
+    assert len(cvsearch._SESSION_CACHE) == 1 and list(cvsearch._SESSION_CACHE.values()) != sess
+    cvsearch.clear_session_cache()
+
+
 def test_small_multi_output_matches_reference(gpu):
     g = golden("small_multi_cv")
     grid = cvsearch.make_grid(float(g["lo"]), float(g["hi"]), int(g["q"]))

@@ -1,7 +1,9 @@
 """Per-launch DRAM traffic and duration of the dominant kernels from an `ncu --set full` report,
 as the JSON bench.py reads for roofline.traffic (profiles/rNN_ncu_top_kernels.json).
 
-    python tools/ncu_top_json.py gpurun_out/top.ncu-rep > profiles/r01_ncu_top_kernels.json
+    python tools/ncu_top_json.py c4=gpurun_out/c4_top.ncu-rep [c5=...] > profiles/r02_ncu_top_kernels.json
+
+Several reports of one config (config=rep, repeated) merge; the output is {config: {kernel: {...}}}.
 """
 
 import csv
@@ -13,7 +15,7 @@ import sys
 KEYS = {"oz_syrk_kernel": "oz_syrk", "oz_syrk_pair_kernel": "oz_syrk", "eval_solve_kernel": "eval_solve", "32, 3>": "holdout_gemm", "oz_dotb_kernel": "oz_holdout", "oz_dotb_pair_kernel": "oz_holdout"}
 
 
-def main(rep):
+def one(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
@@ -41,9 +43,17 @@ def main(rep):
         e["dram_read_bytes"] /= n
         e["dram_write_bytes"] /= n
         e["duration_ms"] /= n
+    return res
+
+
+def main(pairs):
+    res = {}
+    for pair in pairs:
+        cfg, rep = pair.split("=", 1)
+        res.setdefault(cfg, {}).update(one(rep))
     json.dump(res, sys.stdout, indent=1)
     print()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1:])
