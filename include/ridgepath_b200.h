@@ -116,7 +116,10 @@ size_t rp_potrf_workspace_size(int d, int batch);
  *   "chol_ozaki" 0: Cholesky trailing updates on FP64 DMMA (default 1: int8 tensor cores)
  *   "gram_dmma"  1: Gram blocks on FP64 DMMA even with a workspace (default 0)
  *   "holdout_ozaki" 0: Gram-form hold-out on FP64 DMMA (default 1: int8 tensor cores)
- *   "profile"    1: time selected kernels with CUDA events (bench roofline)    */
+ *   "profile"    1: time selected kernels with CUDA events (bench roofline)
+ *   "solve_lam"  n: force the fused solve's lambda chunk (0 = planner)
+ *   "solve_cluster" 2/4/8: fused solve on clusters of that many CTAs sharing each coefficient slab
+ *                (TMA multicast; 0/1 = off, the default: measured slower)                     */
 int rp_set_option(const char* name, int value);
 
 /* Sum of the recorded durations (ms) of kernel `name` ("oz_syrk", "eval_solve",

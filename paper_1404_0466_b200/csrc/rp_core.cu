@@ -33,7 +33,8 @@ int set_error(int code, const char* fmt, ...) {
 }
 
 static std::atomic<long long> g_launches{0};
-extern int g_solve_lam;  // rp_solve.cu
+extern int g_solve_lam;      // rp_solve.cu
+extern int g_solve_cluster;  // rp_solve.cu
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 static bool g_profile = false;
@@ -880,6 +881,12 @@ int rp_set_option(const char* name, int value) {
   }
   if (strcmp(name, "holdout_ozaki") == 0) {
     g_holdout_ozaki = value != 0;
+    return RP_OK;
+  }
+  if (strcmp(name, "solve_cluster") == 0) {
+    RP_REQUIRE(value >= 0 && value <= 8 && (value & (value - 1)) == 0,
+               "rp_set_option: solve_cluster %d (0/1 = off, 2/4/8 = theta multicast clusters)", value);
+    g_solve_cluster = value;
     return RP_OK;
   }
   if (strcmp(name, "solve_lam") == 0) {

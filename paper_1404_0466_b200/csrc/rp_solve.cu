@@ -9,7 +9,8 @@
 using namespace rp;
 
 namespace rp {
-int g_solve_lam = 0;  // rp_set_option("solve_lam", n): 0 = the planner's choice
+int g_solve_lam = 0;      // rp_set_option("solve_lam", n): 0 = the planner's choice
+int g_solve_cluster = 0;  // rp_set_option("solve_cluster", n): 2/4/8 = theta multicast clusters; 0/1 = none
 }
 
 static int launch_generic(int m, const SolveArgs& a, int grid, cudaStream_t st) {
@@ -35,8 +36,59 @@ static int launch_generic(int m, const SolveArgs& a, int grid, cudaStream_t st) 
 
 struct SolvePlan {
   int lam = 0, chunks = 0, S = 0, P = 0, nt = 0;
+  int cl = 1, chunks_pad = 0;  // CTAs per cluster (theta multicast), chunks per fold padded to a multiple of cl
   bool fast = false;
 };
+
+static int generic_clusters(int m, int lam, int P, int cl) {
+  switch (m) {
+    case 1: return solve_clusters<0, 1, 0, 0>(lam, m, P, cl);
+    case 2: return solve_clusters<0, 2, 0, 0>(lam, m, P, cl);
+    case 3: return solve_clusters<0, 3, 0, 0>(lam, m, P, cl);
+    case 4: return solve_clusters<0, 4, 0, 0>(lam, m, P, cl);
+    case 5: return solve_clusters<0, 5, 0, 0>(lam, m, P, cl);
+    case 6: return solve_clusters<0, 6, 0, 0>(lam, m, P, cl);
+    case 7: return solve_clusters<0, 7, 0, 0>(lam, m, P, cl);
+    case 8: return solve_clusters<1, 0, 0, 0>(lam, m, P, cl);
+    case 9: return solve_clusters<1, 1, 0, 0>(lam, m, P, cl);
+    case 10: return solve_clusters<1, 2, 0, 0>(lam, m, P, cl);
+    case 11: return solve_clusters<1, 3, 0, 0>(lam, m, P, cl);
+    case 12: return solve_clusters<1, 4, 0, 0>(lam, m, P, cl);
+    case 13: return solve_clusters<1, 5, 0, 0>(lam, m, P, cl);
+    case 14: return solve_clusters<1, 6, 0, 0>(lam, m, P, cl);
+    case 15: return solve_clusters<1, 7, 0, 0>(lam, m, P, cl);
+    default: return solve_clusters<2, 0, 0, 0>(lam, m, P, cl);
+  }
+}
+
+// Cluster size (on request, rp_set_option("solve_cluster", n)): the CTAs of consecutive chunks of one fold
+// share each theta slab (read once from L2/HBM by rank 0, multicast into every CTA). Padding a fold's
+// chunks to a multiple of cl adds CTAs (copies of the last chunk); the requested size is used when it
+// can be scheduled.
+static void plan_cluster(SolvePlan& pl, int nf, int m, int sms) {
+  pl.cl = 1;
+  pl.chunks_pad = pl.chunks;
+  if (pl.chunks < 2) return;
+  auto clusters = [&](int cl) {
+    return pl.fast ? solve_fast_clusters(m, pl.P, pl.lam, cl) : generic_clusters(m, pl.lam, pl.P, cl);
+  };
+  auto waves = [&](int cl, int active) {
+    const long long ctas = (long long)nf * ((pl.chunks + cl - 1) / cl * cl);
+    return (ctas + active - 1) / active;
+  };
+  const long long base = waves(1, sms);
+  const int force = g_solve_cluster;
+  for (int cl = 8; cl >= 2; cl /= 2) {
+    if (force > 0 && cl != force) continue;
+    if (cl > pl.chunks) continue;
+    const int n = clusters(cl);
+    if (n <= 0) continue;
+    if (force == 0 && waves(cl, n * cl) > base) continue;
+    pl.cl = cl;
+    pl.chunks_pad = (pl.chunks + cl - 1) / cl * cl;
+    return;
+  }
+}
 
 // Chunk size: specialised kernels (full chunks, compile-time P) and the generic kernel compete
 // on the lowest (waves x chunk) cost, the generic kernel's overhead weighted in.
@@ -82,6 +134,11 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
   if (pl.lam > 0) {
     pl.chunks = (q + pl.lam - 1) / pl.lam;
     pl.S = solve_stride(pl.lam, m);
+    // clusters only on request: measured slower at every shape tried (c4 fwd 15.6 -> 18.1 ms at 2 CTAs,
+    // one fold per GPU 14.8 -> 17.7-18.4 ms at 2/4/8): the lockstep refills and the per-row cluster
+    // barrier cost more than the L2/HBM reads they save (the solve is not bandwidth-bound)
+    if (g_solve_cluster > 1) plan_cluster(pl, nf, m, sms);
+    else pl.chunks_pad = pl.chunks;
   }
   return pl;
 }
@@ -122,7 +179,7 @@ extern "C" size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int 
            rp_eval_solve_workspace_size(d, 0, nf, m, 1);
   const SolvePlan pl = plan_solve(d, r, nf, m, q);
   if (pl.lam == 0) return 0;
-  return sizeof(double) * (size_t)nf * pl.chunks * (size_t)pl.nt * 64 * pl.S;
+  return sizeof(double) * (size_t)nf * pl.chunks_pad * (size_t)pl.nt * 64 * pl.S;
 }
 
 extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m,
@@ -198,7 +255,9 @@ static int eval_solve_planned(const double* theta, int d, int r, int nf, const d
   a.nt = nt;
   a.P = P;
   a.lam_per_cta = pl.lam;
-  a.chunks = pl.chunks;
+  a.chunks = pl.chunks_pad;
+  a.chunks_real = pl.chunks;
+  a.cl = pl.cl;
   a.S = pl.S;
   a.Wc = (double*)work;
   const int grid = nf * a.chunks;

@@ -63,6 +63,9 @@ struct SolveArgs {
   int* flags;
   int flag_stride;  // flags of fold f at flags + f * flag_stride (q unless a caller splits the grid)
   int q, m, d, nt, P, lam_per_cta, chunks, S;
+  int chunks_real;  // chunks that cover the grid; chunks (>= chunks_real, a multiple of cl) pads the
+                    // last cluster of a fold with copies of its last chunk (bit-identical duplicate writes)
+  int cl;           // CTAs per cluster: consecutive chunks of one fold; rank 0 multicasts the theta slabs
   double* Wc;      // chunk-private rows of the solution (dp x S per CTA)
   int64_t ntiles;  // 64 x 64 tiles per fold
 };
@@ -107,6 +110,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
   double* sR = smem + (ring > diagw ? ring : diagw);
   uint64_t* full = reinterpret_cast<uint64_t*>(sR + 64 * S);  // per stage, + [STG] diagonal tile
   uint64_t* empty = full + STG + 1;                             // per stage: all warps released it
+  uint64_t* cempty = empty + STG;  // per stage, used in cluster rank 0: all warps of the cluster released it
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -117,7 +121,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
   auto slab_row = [&](int mt) {
     return BWD ? rg * 16 + mt * 8 + (g >> 1) + 4 * (g & 1) : rg * 16 + 2 * g + mt;
   };
-  const int fold = blockIdx.x / a.chunks, chunk = blockIdx.x % a.chunks;
+  const int fold = blockIdx.x / a.chunks, chunk = min((int)(blockIdx.x % a.chunks), a.chunks_real - 1);
+  const int cl = a.cl;
+  const uint32_t rank = cl > 1 ? cluster_rank() : 0;
   const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
   const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
   if (nl <= 0) return;
@@ -129,9 +135,12 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
   if (tid == 0) {
     for (int i = 0; i <= STG; ++i) mbar_init(&full[i], 1);
     for (int i = 0; i < STG; ++i) mbar_init(&empty[i], NTH / 32);
+    for (int i = 0; i < STG; ++i) mbar_init(&cempty[i], NTH / 32 * cl);
     fence_mbar_init();
   }
   __syncthreads();
+  if (cl > 1) cluster_sync();  // every CTA's barriers are initialised before any remote arrival
+  const uint32_t cempty0 = cl > 1 ? cluster_addr(cempty, 0) : 0;  // rank 0's cluster-release barriers
   int it0 = 0;  // slabs consumed by earlier rows (stage / phase bookkeeping)
 
 #ifdef RP_SOLVE_PROF
@@ -177,6 +186,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
     // 128-byte swizzle) + the 16 already solved rows of this CTA's private W, completion on full[st].
     // A stage is refilled once every warp has released its previous slab (empty[st]); only the
     // issuing thread waits for that, the other warps run ahead as far as the data allows.
+    // In a cluster (cl > 1, the CTAs of consecutive lambda chunks of one fold) rank 0 reads each theta
+    // slab once and multicasts it into every CTA's stage, after every warp of the cluster released that
+    // stage (cempty); each CTA still copies its own W rows.
     auto issue = [&](int s) {
       if (tid == 0 && s < nslab) {
         const int it = it0 + s, st = it % STG;
@@ -185,27 +197,37 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
         const int kq = s & 3;
         const uint32_t bytes = (uint32_t)(stageT * 8 + 16 * S * 8);
         mbar_arrive_expect_tx(&full[st], bytes);
-        if (BWD) {
-          const int64_t row0 = fold * a.theta_fold_stride / TILE_LD + (int64_t)tile_index(J, I) * P * 64;
-          for (int p = 0; p < P; ++p)
-            tma_2d_g2s(sT + st * stageT + p * BWD_SLAB, &a.tmb, kq * 16, (int)(row0 + p * 64), &full[st]);
-        } else {
-          const double* tile = theta + (int64_t)tile_index(I, J) * P * TILE_PLANE;
-          for (int p = 0; p < P; ++p)
-            bulk_g2s(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
-                     (uint32_t)(FWD_SLAB * 8), &full[st]);
+        if (rank == 0) {
+          const uint16_t mask = (uint16_t)((1u << cl) - 1u);
+          if (cl > 1 && it >= STG) mbar_wait_cluster(&cempty[st], ((it / STG) + 1) & 1);
+          if (BWD) {
+            const int64_t row0 = fold * a.theta_fold_stride / TILE_LD + (int64_t)tile_index(J, I) * P * 64;
+            for (int p = 0; p < P; ++p) {
+              if (cl > 1)
+                tma_2d_g2s_multicast(sT + st * stageT + p * BWD_SLAB, &a.tmb, kq * 16, (int)(row0 + p * 64),
+                                     &full[st], mask);
+              else
+                tma_2d_g2s(sT + st * stageT + p * BWD_SLAB, &a.tmb, kq * 16, (int)(row0 + p * 64), &full[st]);
+            }
+          } else {
+            const double* tile = theta + (int64_t)tile_index(I, J) * P * TILE_PLANE;
+            for (int p = 0; p < P; ++p) {
+              if (cl > 1)
+                bulk_g2s_multicast(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
+                                   (uint32_t)(FWD_SLAB * 8), &full[st], mask);
+              else
+                bulk_g2s(sT + st * stageT + p * FWD_SLAB, tile + p * TILE_PLANE + kq * 16 * TILE_LD,
+                         (uint32_t)(FWD_SLAB * 8), &full[st]);
+            }
+          }
         }
         bulk_g2s(sW + st * stageW, Wc + (int64_t)(J * 64 + kq * 16) * S, (uint32_t)(16 * S * 8), &full[st]);
       }
     };
 
-#ifndef RP_SOLVE_AHEAD_BWD
-#define RP_SOLVE_AHEAD_BWD 2
-#endif
-#ifndef RP_SOLVE_AHEAD_FWD
-#define RP_SOLVE_AHEAD_FWD 2
-#endif
-    constexpr int AHEAD = BWD ? RP_SOLVE_AHEAD_BWD : RP_SOLVE_AHEAD_FWD;  // slabs in flight ahead of the consumers
+    // slabs in flight ahead of the consumers: 2 with the 3/4-stage rings of the large chunks (compute
+    // per slab hides the copy latency), STG - 2 with the deep rings of small chunks (latency-bound)
+    constexpr int AHEAD = STG >= 6 ? STG - 2 : 2;
 #pragma unroll
     for (int s0 = 0; s0 < AHEAD; ++s0) issue(s0);
 #pragma unroll 1
@@ -220,72 +242,95 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
       //  bwd: its k values of the k-steps 2 kp and 2 kp + 1 are adjacent (k = 8 kp + 2 t + h), one
       //       swizzled 16-byte chunk of row slab_row(mt), chunk index (4 kp + t) ^ (row & 7).
       // Both are bank-conflict free, and the B fragments (W rows k) stay conflict free (S = 12 mod 16).
+      // k-step ks (0..3) of the slab, with the coefficient fragments of its two m-tiles in th[mt][plane]
+      auto kstep = [&](int ks, const double (&th)[2][PM]) {
+        const double* wrow = Wb + (BWD ? 8 * (ks >> 1) + 4 * (ks & 1) + t : ks * 4 + t) * S;
 #pragma unroll
-      for (int kp = 0; kp < 2; ++kp) {
-        double th[2][2][PM];  // [h: k-step 2 kp + h][mt][plane]
+        for (int i = 0; i < LH; ++i) {
+          const int l = lg * LH + i;
+          if (l < nl) {
+            double b[NTA];
+            double rv[REMA];
 #pragma unroll
-        for (int p = 0; p < PM; ++p) {
-          if (p < P) {
-            if (BWD) {
+            for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
+            if (REM2) {
+#pragma unroll
+              for (int c = 0; c < REM; c += 2) {
+                const double2 v2 = *reinterpret_cast<const double2*>(wrow + l * m + NT * 8 + c);
+                rv[c] = v2.x;
+                rv[c + 1] = v2.y;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+              // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
+              double av = 0.0;
+#pragma unroll
+              for (int p = PM - 1; p >= 0; --p)
+                if (p < P) av = (p == P - 1) ? th[mt][p] : fma(av, tl[i], th[mt][p]);
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
+#pragma unroll
+              for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+            }
+          }
+        }
+      };
+      if (!BWD) {
+        // forward: one 16-byte load per (k-step, plane) holds both m-tiles' rows; the next k-step's
+        // fragments are loaded while this one computes
+        auto ldf = [&](int ks, double (&th)[2][PM]) {
+#pragma unroll
+          for (int p = 0; p < PM; ++p)
+            if (p < P) {
+              const double2 v =
+                  *reinterpret_cast<const double2*>(T + p * FWD_SLAB + (ks * 4 + t) * 68 + slab_row(0));
+              th[0][p] = v.x;
+              th[1][p] = v.y;
+            }
+        };
+        double tha[2][PM], thb[2][PM];
+        ldf(0, tha);
+        ldf(1, thb);
+        kstep(0, tha);
+        ldf(2, tha);
+        kstep(1, thb);
+        ldf(3, thb);
+        kstep(2, tha);
+        kstep(3, thb);
+      } else {
+        // backward: one 16-byte load per (m-tile, plane) holds two k-steps (swizzled row chunk); the
+        // second pair is loaded while the first computes
+        auto ldb = [&](int kp, double (&th0)[2][PM], double (&th1)[2][PM]) {
+#pragma unroll
+          for (int p = 0; p < PM; ++p)
+            if (p < P) {
 #pragma unroll
               for (int mt = 0; mt < 2; ++mt) {
                 const int row = slab_row(mt);
                 const double2 v = *reinterpret_cast<const double2*>(
                     T + p * BWD_SLAB + row * 16 + (((4 * kp + t) ^ (row & 7)) << 1));
-                th[0][mt][p] = v.x;
-                th[1][mt][p] = v.y;
-              }
-            } else {
-#pragma unroll
-              for (int h = 0; h < 2; ++h) {
-                const double2 v = *reinterpret_cast<const double2*>(
-                    T + p * FWD_SLAB + ((2 * kp + h) * 4 + t) * 68 + slab_row(0));
-                th[h][0][p] = v.x;
-                th[h][1][p] = v.y;
+                th0[mt][p] = v.x;
+                th1[mt][p] = v.y;
               }
             }
-          }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const double* wrow = Wb + (BWD ? 8 * kp + 4 * h + t : (2 * kp + h) * 4 + t) * S;
-#pragma unroll
-          for (int i = 0; i < LH; ++i) {
-            const int l = lg * LH + i;
-            if (l < nl) {
-              double b[NTA];
-#pragma unroll
-              for (int j = 0; j < NT; ++j) b[j] = wrow[l * m + j * 8 + g];
-              double rv[REMA];
-              if (REM2) {
-#pragma unroll
-                for (int c = 0; c < REM; c += 2) {
-                  const double2 v2 = *reinterpret_cast<const double2*>(wrow + l * m + NT * 8 + c);
-                  rv[c] = v2.x;
-                  rv[c + 1] = v2.y;
-                }
-              } else {
-#pragma unroll
-                for (int c = 0; c < REM; ++c) rv[c] = wrow[l * m + NT * 8 + c];
-              }
-#pragma unroll
-              for (int mt = 0; mt < 2; ++mt) {
-                // Horner from the top plane: v = theta_{P-1}; v = v*t + theta_p
-                double av = 0.0;
-#pragma unroll
-                for (int p = PM - 1; p >= 0; --p)
-                  if (p < P) av = (p == P - 1) ? th[h][mt][p] : fma(av, tl[i], th[h][mt][p]);
-#pragma unroll
-                for (int j = 0; j < NT; ++j) dmma884(acc[i][mt][j][0], acc[i][mt][j][1], av, b[j]);
-#pragma unroll
-                for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
-              }
-            }
-          }
-        }
+        };
+        double th0[2][PM], th1[2][PM], th2[2][PM], th3[2][PM];
+        ldb(0, th0, th1);
+        ldb(1, th2, th3);
+        kstep(0, th0);
+        kstep(1, th1);
+        kstep(2, th2);
+        kstep(3, th3);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) {
+        mbar_arrive(&empty[st]);
+        if (cl > 1) mbar_arrive_cluster(cempty0 + 8u * st);
+      }
     }
     it0 += nslab;
     __syncthreads();  // every warp is done with the ring
@@ -486,6 +531,9 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
     }
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
     __syncthreads();
+    // the diagonal step used the ring's memory: rank 0 multicasts the next row's slabs only after every
+    // CTA of the cluster is done with it
+    if (cl > 1) cluster_sync();
     RP_SP_MARK(5);  // publish
   }
 #ifdef RP_SOLVE_PROF
@@ -509,7 +557,8 @@ inline size_t solve_smem_bytes(int lam, int m, int P, int stages = SOLVE_STAGES,
   size_t ring = stages * per_stage;
   // theta_II + the evaluated 16 x 16 diagonal blocks + pivots, in the idle ring during the diagonal step
   size_t diag = (size_t)P * TILE_PLANE + (size_t)lam * (16 * 17 + 16);
-  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 16) + (bwd ? 1024 : 0);  // + mbarriers
+  // + mbarriers: full (stages + 1), empty and cluster-empty (stages each)
+  return sizeof(double) * ((ring > diag ? ring : diag) + 64 * (size_t)S + 3 * (size_t)stages + 1) + (bwd ? 1024 : 0);
 }
 
 inline size_t solve_smem_max(int lam, int m, int P, int stages = SOLVE_STAGES) {
@@ -517,6 +566,28 @@ inline size_t solve_smem_max(int lam, int m, int P, int stages = SOLVE_STAGES) {
   return f > b ? f : b;
 }
 
+
+template <typename K>
+static cudaError_t launch_clustered(K kern, int grid, int threads, size_t smem, int cl, cudaStream_t st,
+                                   const SolveArgs& a) {
+  if (cl <= 1) {
+    kern<<<grid, threads, smem, st>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
+}
 
 template <int NT, int REM, int PT, int LCT, int LG = 2, int STG = SOLVE_STAGES>
 int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
@@ -526,21 +597,58 @@ int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
   const size_t sb = solve_smem_bytes(a.lam_per_cta, a.m, a.P, STG, true);
   cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sf);
   cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+  if (a.cl > 8) {
+    cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
   {
     ProfScope prof("eval_solve_fwd", st);
-    kf<<<grid, 128 * LG, sf, st>>>(a);
+    cudaError_t e = launch_clustered(kf, grid, 128 * LG, sf, a.cl, st, a);
+    if (e != cudaSuccess) return cuda_status(e, "eval_solve fwd launch");
   }
   RP_LAUNCH_CHECK("eval_solve fwd");
   {
     ProfScope prof("eval_solve_bwd", st);
-    kb<<<grid, 128 * LG, sb, st>>>(a);
+    cudaError_t e = launch_clustered(kb, grid, 128 * LG, sb, a.cl, st, a);
+    if (e != cudaSuccess) return cuda_status(e, "eval_solve bwd launch");
   }
   RP_LAUNCH_CHECK("eval_solve bwd");
   return RP_OK;
 }
 
+// Co-resident clusters of `cl` CTAs (the smaller of the two passes; 0 when the shape cannot be scheduled).
+template <int NT, int REM, int PT, int LCT, int LG = 2, int STG = SOLVE_STAGES>
+int solve_clusters(int lam, int m, int P, int cl) {
+  int best = 1 << 30;
+  for (int bwd = 0; bwd < 2; ++bwd) {
+    auto k = bwd ? eval_solve_kernel<NT, REM, PT, LCT, LG, STG, true> : eval_solve_kernel<NT, REM, PT, LCT, LG, STG, false>;
+    const size_t smem = solve_smem_bytes(lam, m, P, STG, bwd);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cl > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(128 * LG);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    best = n < best ? n : best;
+  }
+  return best;
+}
+
 // Fast instantiations (rp_solve_fast.cu): returns -2 when (m, P, lam) has none.
 int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st);
 bool has_solve_fast(int m, int P, int lam);
+int solve_fast_clusters(int m, int P, int lam, int cl);  // solve_clusters of that instantiation
 
 }  // namespace rp

@@ -22,15 +22,43 @@ bool has_solve_fast(int m, int P, int lam) {
   return false;
 }
 
-// 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4; a 4-stage
-// ring (two slabs per barrier phase) when it fits in shared memory.
+// 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4. Ring depth:
+// small chunks (<= 4 lambdas: little arithmetic per slab, e.g. the one-fold-per-GPU case) are bound by
+// the copy latency and get a 6-stage ring with 4 slabs in flight when it fits; otherwise a 4-stage ring
+// (two slabs in flight) when it fits, else 3 stages.
 template <int M, int P, int LC>
-static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st) {
+static int stages_fast() {
   int dev = 0, maxsm = 227 * 1024;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  if (solve_smem_max(LC, M, P, 4) <= (size_t)maxsm) return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, st);
-  return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, st);
+  if (LC <= 4 && solve_smem_max(LC, M, P, 6) <= (size_t)maxsm) return 6;
+  return solve_smem_max(LC, M, P, 4) <= (size_t)maxsm ? 4 : 3;
+}
+
+template <int M, int P, int LC>
+static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st) {
+  switch (stages_fast<M, P, LC>()) {
+    case 6: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, (LC <= 4 ? 6 : 4)>(a, grid, st);
+    case 4: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, st);
+    default: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, st);
+  }
+}
+
+template <int M, int P, int LC>
+static int clusters_fast(int cl) {
+  switch (stages_fast<M, P, LC>()) {
+    case 6: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, (LC <= 4 ? 6 : 4)>(LC, M, P, cl);
+    case 4: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(LC, M, P, cl);
+    default: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(LC, M, P, cl);
+  }
+}
+
+int solve_fast_clusters(int m, int P, int lam, int cl) {
+#define RP_CL(M, PP, L) \
+  if (m == M && P == PP && lam == L) return clusters_fast<M, PP, L>(cl);
+  RP_FAST_LIST(RP_CL)
+#undef RP_CL
+  return 0;
 }
 
 int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st) {

@@ -191,6 +191,55 @@ def test_eval_solve_bit_identical_across_chunkings(gpu, solve_lam, m, r, lams):
         assert np.array_equal(W, base)
 
 
+@pytest.fixture
+def solve_cluster():
+    yield lambda v: call("rp_set_option", b"solve_cluster", v)
+    call("rp_set_option", b"solve_cluster", 0)
+
+
+@pytest.mark.parametrize("m,r,lam", [(10, 2, 2), (10, 2, 12), (1, 2, 8), (16, 3, 8), (3, 2, 0)])
+@pytest.mark.parametrize("nf", [1, 3])
+def test_eval_solve_clusters_bit_identical(gpu, solve_lam, solve_cluster, m, r, lam, nf):
+    """Theta slabs multicast across a cluster of 2/4/8 CTAs (consecutive chunks of one fold, the fold's
+    last cluster padded with copies of its last chunk): solutions bit-identical to the unclustered
+    solve, every fold and chunk, with W, flags and the (larger, padded) workspace in red zones."""
+    d = 200
+    q = 41 if m % 2 == 0 else 42
+    H, lams_s, tiles1, G, ts, tsh = _solve_setup(d, r, m, seed=40 + m)
+    torch = _dev.torch()
+    te = tile_elems(d, r + 1)
+    tiles = _dev.empty((nf * te,))
+    for f in range(nf):  # fold f: the same factors scaled by (1 + f), so every fold's solution differs
+        tiles[f * te:(f + 1) * te].copy_(tiles1.reshape(-1)[:te] * (1.0 + f))
+    grid = np.logspace(-2, 0, q)
+    tv = ts * grid + tsh
+    dp = padded(d)
+    rhs = _dev.zeros((nf, dp, m))
+    rhs[:, :d].copy_(torch.from_numpy(np.ascontiguousarray(G)).unsqueeze(0))
+    ldw = q * m + ((q * m) & 1)
+    if lam:
+        solve_lam(lam)
+
+    def run(cl):
+        solve_cluster(cl)
+        W = Guarded(nf * dp * ldw)
+        fl = Guarded(nf * q)
+        ws = guarded_ws(_lib.query("rp_eval_solve_workspace_size", d, r, nf, m, q))
+        call("rp_eval_solve", ptr(tiles), d, r, nf, ptr(rhs), m, ptr(_dev.to_dev(tv)), q, ptr(W.buf), ldw,
+             ptr(fl.buf), ptr(ws.buf), stream())
+        assert W.margins_intact() and fl.margins_intact() and ws.margins_intact(), f"cluster {cl}"
+        return W.buf.cpu().numpy().reshape(nf, dp, ldw)[:, :d, :q * m].copy()
+
+    base = run(1)
+    mod = orc.fit(H, lams_s, r)
+    for f in range(nf):
+        Wf = base[f].reshape(d, q, m)
+        for j in (0, q // 2, q - 1):  # L scaled by (1+f): W = (LL^T)^-1 G / (1+f)^2
+            assert rel(Wf[:, j] * (1.0 + f) ** 2, orc.solve_interp(mod, G, grid[j])) <= 1e-10
+    for cl in (2, 4, 8):
+        assert np.array_equal(run(cl), base), f"cluster {cl} differs"
+
+
 def test_generic_solve_matches_specialised_bitwise(gpu):
     """m = 10 with an odd grid size runs the generic kernel for some chunkings; its arithmetic per lambda is
     the specialised kernel's, so results are bit-identical to the fast path on the shared lambdas."""

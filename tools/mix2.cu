@@ -29,6 +29,8 @@ __global__ void __launch_bounds__(512, 1) mix884(double* out, int iters, double 
   double acc[U][2], accx[U][REM > 0 ? REM : 1], av[U];
   double th[P], tl[U], b = 1.0 - threadIdx.x * 1e-5, rv[REM > 0 ? REM : 1];
 #pragma unroll
+  for (int u = 0; u < U; ++u) av[u] = 0.5 + u;
+#pragma unroll
   for (int p = 0; p < P; ++p) th[p] = threadIdx.x * 1e-3 + p;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
@@ -60,6 +62,25 @@ __global__ void __launch_bounds__(512, 1) mix884(double* out, int iters, double 
 #pragma unroll
         for (int c = 0; c < REM; ++c) accx[u][c] = vfma(a, rv[c], accx[u][c]);
       }
+    } else if (MODE == 3) {
+      // software-pipelined: this iteration's DMMAs / leftovers consume the values evaluated in the previous
+      // iteration; this iteration's Horner results are only needed by the next one
+      double an[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        double a = th[P - 1];
+#pragma unroll
+        for (int p = P - 2; p >= 0; --p) a = fma(a, tl[u], th[p]);
+        an[u] = a;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        dmma884(acc[u][0], acc[u][1], av[u], b);
+#pragma unroll
+        for (int c = 0; c < REM; ++c) accx[u][c] = fma(av[u], rv[c], accx[u][c]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) av[u] = an[u];
     } else {
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -185,16 +206,16 @@ int main() {
   cudaMalloc(&out, 1 << 20);
   run884<6, 1, 0, 0>(sms, out, 512);  // DMMA only
   run884<6, 3, 0, 0>(sms, out, 512);  // Horner + DMMA
+  run884<6, 3, 0, 3>(sms, out, 512);
   run884<6, 1, 2, 0>(sms, out, 512);  // DMMA + leftover
   run884<6, 3, 2, 0>(sms, out, 512);
-  run884<6, 3, 2, 1>(sms, out, 512);
-  run884<6, 3, 2, 2>(sms, out, 512);
-  run884<6, 3, 2, 0>(sms, out, 256);
-  run884<12, 3, 2, 0>(sms, out, 256);
-  run884<12, 3, 2, 2>(sms, out, 256);
+  run884<6, 3, 2, 3>(sms, out, 512);
+  run884<6, 3, 2, 3>(sms, out, 256);
+  run884<12, 3, 2, 3>(sms, out, 256);
+  run884<12, 3, 2, 3>(sms, out, 384);
+  run884<8, 3, 2, 3>(sms, out, 384);
+  run884<4, 3, 2, 3>(sms, out, 512);
   run884<6, 4, 0, 0>(sms, out, 512);   // c5: degree 3, m = 16 -> 2 DMMA per element, no leftover
-  run16816<2, 3, 2>(sms, out, 512);
-  run16816<3, 3, 2>(sms, out, 256);
-  run16816<2, 1, 0>(sms, out, 512);
+  run884<6, 4, 0, 3>(sms, out, 512);
   return 0;
 }

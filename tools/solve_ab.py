@@ -19,6 +19,9 @@ cfg = configs.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c4"]
 X, Y = configs.generate(cfg)
 grid = configs.grid_values(cfg)
 sess = cvsearch.CvSession([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, grid, g=cfg.s, r=cfg.r)
+for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=solve_cluster=2
+    k, v = kv.split("=")
+    _lib.call("rp_set_option", k.encode(), int(v))
 sess.upload(X, Y)
 for _ in range(3):
     sess.sweep()
@@ -31,4 +34,4 @@ for rep in range(5):
     for n in ("eval_solve", "eval_solve_fwd", "eval_solve_bwd", "oz_syrk"):
         res.setdefault(n, []).append(_lib.query("rp_profile_ms", n.encode()))
     res.setdefault("all", []).append(_lib.query("rp_profile_ms", None))
-print(os.path.basename(sys.argv[1]), {k: round(float(np.median(v)), 3) for k, v in res.items()})
+print(os.path.basename(sys.argv[1]), os.environ.get("RP_OPTS", ""), {k: round(float(np.median(v)), 3) for k, v in res.items()})

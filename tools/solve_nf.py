@@ -1,4 +1,5 @@
 """Solve time of the c4 sweep for a subset of local folds (the per-rank work at N GPUs)."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -17,6 +18,9 @@ from paper_1404_0466_b200.engine import PicholEngine  # noqa: E402
 eng = PicholEngine([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, cfg.q, sess.lams.shape[0], cfg.r,
                    local_folds=shard.local_folds)
 sess.engine = eng
+for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=solve_cluster=8
+    k, v = kv.split("=")
+    _lib.call("rp_set_option", k.encode(), int(v))
 sess.upload(torch.from_numpy(X), torch.from_numpy(Y))
 for _ in range(2):
     sess.sweep()
@@ -27,6 +31,6 @@ for _ in range(3):
 _lib.call("rp_set_option", b"profile", 1)
 _lib.query("rp_profile_ms", None)
 sess.sweep()
-solve = _lib.query("rp_profile_ms", b"eval_solve")
+solve = _lib.query("rp_profile_ms", b"eval_solve_fwd") + _lib.query("rp_profile_ms", b"eval_solve_bwd")
 _lib.call("rp_set_option", b"profile", 0)
-print(f"world={world} local={shard.local_folds} stages(ms)={ {k: round(v * 1e3, 2) for k, v in tim.items()} } solve_kernel={solve:.2f}")
+print(f"opts={os.environ.get('RP_OPTS', '')} world={world} local={shard.local_folds} stages(ms)={ {k: round(v * 1e3, 2) for k, v in tim.items()} } solve_kernel={solve:.2f}")
