@@ -237,13 +237,22 @@ struct FitArgs {
 };
 
 // theta_p = sum_s P[p][s] L_s for one 64 x 64 tile (I, J) of every fold, written straight into the
-// column-major padded tile planes (consecutive threads on consecutive rows: coalesced reads of the
-// factors and writes of the planes), with the tile's share of ||T - V theta||_F^2. Padding rows
-// (64..67) and entries outside the triangle are 0, padded diagonal entries 1 in plane 0.
-template <int SMAX>
-__global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, int s, int r, int64_t ntiles,
-                                                        int64_t fold_stride, FitArgs fa, double* theta,
-                                                        double* partial) {
+// column-major padded tile planes, with the tile's share of ||T - V theta||_F^2. Padding rows (64..67)
+// and entries outside the triangle are 0, padded diagonal entries 1 in plane 0.
+// HBM-bound (s factor reads + P plane writes per entry): each thread owns pairs of adjacent rows of a
+// column (16-byte loads of every factor and 16-byte streaming stores of every plane, coalesced along
+// the column), and the kernel is sized for 4 resident CTAs per SM so enough loads are in flight to
+// cover the HBM latency.
+constexpr int FIT_THREADS = 256;
+constexpr int FIT_PAIRS = TILE_PLANE / 2;  // 34 row pairs (64 rows + 4 padding) per column x 64 columns
+
+// Occupancy over unrolling (measured at c4, ms): 4 CTAs x 256 threads per SM, one pair per thread in
+// flight 0.95; 2 CTAs with 2 / 3 pairs in flight 1.22 / 1.21; 3 CTAs x 2 pairs 1.10; 5 / 6 / 8 CTAs
+// (register-capped) 1.08 / 1.17 / 1.63.
+template <int SMAX, int FIT_UNROLL = 1>
+__global__ void __launch_bounds__(FIT_THREADS, SMAX <= 8 ? 4 : 1) fit_tiles_kernel(const double* L, int d, int s, int r,
+                                                                int64_t ntiles, int64_t fold_stride, FitArgs fa,
+                                                                double* theta, double* partial) {
   const int64_t tile = blockIdx.x;
   const int f = blockIdx.y;
   const int P = r + 1;
@@ -254,46 +263,98 @@ __global__ void __launch_bounds__(512) fit_tiles_kernel(const double* L, int d, 
   const int64_t n = (int64_t)d * d;
   const double* Lf = L + (int64_t)f * s * n;
   double* out = theta + f * fold_stride + tile * P * TILE_PLANE;
+  const bool vec = (d & 1) == 0 && ((uintptr_t)L & 15) == 0;  // 16-byte aligned row pairs in the factors
   double res = 0.0;
-  for (int e = threadIdx.x; e < TILE_PLANE; e += blockDim.x) {
-    const int j = e / TILE_LD, i = e - j * TILE_LD;  // (row i, col j) of the tile
-    const int row = I * 64 + i, col = J * 64 + j;
-    if (i < 64 && row < d && col < d && row >= col) {
-      double T[SMAX];
+  for (int q0 = threadIdx.x; q0 < FIT_PAIRS; q0 += FIT_THREADS * FIT_UNROLL) {
+    double2 T[FIT_UNROLL][SMAX];
+    int kind[FIT_UNROLL];  // 0: outside the tile, 1: both rows in the triangle, 2: mixed (edge / diagonal)
 #pragma unroll
-      for (int si = 0; si < SMAX; ++si) T[si] = (si < s) ? __ldcs(Lf + si * n + (int64_t)col * d + row) : 0.0;
-      double th[5];
+    for (int u = 0; u < FIT_UNROLL; ++u) {
+      const int qq = q0 + u * FIT_THREADS;
+      const int e = 2 * qq;
+      const int j = e / TILE_LD, i = e - j * TILE_LD;  // rows i, i + 1 of column j of the tile
+      const int row = I * 64 + i, col = J * 64 + j;
+      const bool in0 = qq < FIT_PAIRS && i < 64 && row < d && col < d && row >= col;
+      const bool in1 = qq < FIT_PAIRS && i + 1 < 64 && row + 1 < d && col < d && row + 1 >= col;
+      kind[u] = (in0 && in1 && vec) ? 1 : ((in0 || in1) ? 2 : 0);
+      const double* src = Lf + (int64_t)col * d + row;
+#pragma unroll
+      for (int si = 0; si < SMAX; ++si) {
+        if (si < s && kind[u] == 1) {
+          T[u][si] = __ldcs(reinterpret_cast<const double2*>(src + si * n));
+        } else if (si < s && kind[u] == 2) {
+          T[u][si].x = in0 ? __ldcs(src + si * n) : 0.0;
+          T[u][si].y = in1 ? __ldcs(src + si * n + 1) : 0.0;
+        } else {
+          T[u][si] = make_double2(0.0, 0.0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < FIT_UNROLL; ++u) {
+      const int qq = q0 + u * FIT_THREADS;
+      if (qq >= FIT_PAIRS) continue;
+      const int e = 2 * qq;
+      if (kind[u] == 0) {
+        const int j = e / TILE_LD, i = e - j * TILE_LD;
+        const int row = I * 64 + i, col = J * 64 + j;
+        const double d0 = (i < 64 && row == col && row >= d) ? 1.0 : 0.0;
+        const double d1 = (i + 1 < 64 && row + 1 == col && row + 1 >= d) ? 1.0 : 0.0;
+        for (int p = 0; p < P; ++p)
+          __stcs(reinterpret_cast<double2*>(out + p * TILE_PLANE + e), p == 0 ? make_double2(d0, d1)
+                                                                             : make_double2(0.0, 0.0));
+        continue;
+      }
+      // rows outside the triangle (mixed pairs) carry T = 0 and get theta = 0 and no residual
+      const int j = e / TILE_LD, i = e - j * TILE_LD;
+      const int row = I * 64 + i, col = J * 64 + j;
+      const bool in0 = i < 64 && row < d && col < d && row >= col;
+      const bool in1 = i + 1 < 64 && row + 1 < d && col < d && row + 1 >= col;
+      double2 th[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
         if (p < P) {
-          double v = 0.0;
+          double v0 = 0.0, v1 = 0.0;
 #pragma unroll
           for (int si = 0; si < SMAX; ++si)
-            if (si < s) v = fma(fa.P[p][si], T[si], v);
-          th[p] = v;
-          __stcs(out + p * TILE_PLANE + e, v);
+            if (si < s) {
+              v0 = fma(fa.P[p][si], T[u][si].x, v0);
+              v1 = fma(fa.P[p][si], T[u][si].y, v1);
+            }
+          th[p] = make_double2(v0, v1);
+          if (kind[u] == 2) {  // padded diagonal entries below d keep the identity in plane 0
+            if (!in0) th[p].x = (p == 0 && i < 64 && row == col && row >= d) ? 1.0 : 0.0;
+            if (!in1) th[p].y = (p == 0 && i + 1 < 64 && row + 1 == col && row + 1 >= d) ? 1.0 : 0.0;
+          }
+          __stcs(reinterpret_cast<double2*>(out + p * TILE_PLANE + e), th[p]);
         }
       }
 #pragma unroll
       for (int si = 0; si < SMAX; ++si) {
         if (si < s) {
-          double v = 0.0;
+          double v0 = 0.0, v1 = 0.0;
 #pragma unroll
           for (int p = 0; p < 5; ++p)
-            if (p < P) v = fma(fa.V[si][p], th[p], v);
-          const double dlt = T[si] - v;
-          res = fma(dlt, dlt, res);
+            if (p < P) {
+              v0 = fma(fa.V[si][p], th[p].x, v0);
+              v1 = fma(fa.V[si][p], th[p].y, v1);
+            }
+          if (in0) {
+            const double dl = T[u][si].x - v0;
+            res = fma(dl, dl, res);
+          }
+          if (in1) {
+            const double dl = T[u][si].y - v1;
+            res = fma(dl, dl, res);
+          }
         }
       }
-    } else {
-      const double diag = (i < 64 && row == col && row >= d) ? 1.0 : 0.0;
-      for (int p = 0; p < P; ++p) __stcs(out + p * TILE_PLANE + e, (p == 0) ? diag : 0.0);
     }
   }
-  __shared__ double red[512];
+  __shared__ double red[FIT_THREADS];
   red[threadIdx.x] = res;
   __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+  for (int w = FIT_THREADS / 2; w > 0; w >>= 1) {
     if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
@@ -1034,6 +1095,7 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
                  double* theta, double* resid, void* work, void* stream) {
   RP_REQUIRE(d >= 1 && nf >= 1 && s >= 1 && r >= 0 && s > r, "rp_fit_tiles: bad sizes d=%d nf=%d s=%d r=%d", d, nf,
              s, r);
+  RP_REQUIRE(((uintptr_t)theta & 15) == 0, "rp_fit_tiles: theta must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nt = rp_tile_count(d);
   double* partial = (double*)work;
@@ -1045,12 +1107,17 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
         fa.P[p][i] = P_host[p * s + i];
         fa.V[i][p] = V_host[i * (r + 1) + p];
       }
-    if (s <= 8)
-      fit_tiles_kernel<8><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
-                                                                   partial);
+    const dim3 grid((unsigned)nt, nf);
+    const int64_t fs = rp_theta_size(d, r);
+    if (s <= 4)
+      fit_tiles_kernel<4><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
+    else if (s <= 6)
+      fit_tiles_kernel<6><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
+    else if (s <= 8)
+      fit_tiles_kernel<8><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
     else
-      fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), 512, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa, theta,
-                                                                    partial);
+      fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), FIT_THREADS, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa,
+                                                                            theta, partial);
   } else {
     double* Pd = partial + (size_t)nt * nf;
     double* Vd = Pd + (size_t)s * (r + 1);
