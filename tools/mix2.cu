@@ -2,6 +2,7 @@
 // (Horner DFMA -> DMMA + leftover DFMA) depending on instruction order and MMA shape.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mix2 tools/mix2.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
@@ -167,7 +168,12 @@ static float time_it(K kern, int sms, int threads, double* out, int iters) {
   kern<<<sms, threads>>>(out, iters, 0.3);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
-  float ms;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    printf("CUDA error %s\n", cudaGetErrorString(err));
+    exit(1);
+  }
+  float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   return ms;
 }
@@ -199,23 +205,107 @@ static void run16816(int sms, double* out, int threads) {
   report(name, ms, 2048.0 * U, 8.0 * U * (P - 1 + REM), sms, threads, iters);
 }
 
+
+// MODE-4 kernel: the solve's per-warp k-step structure with operands from shared memory: 2 m-tiles with
+// their own P coefficient values (one 16-byte load per plane), LH lambdas each with its own B value and
+// REM leftover values (loaded per k-step), Horner per (lambda, m-tile), DMMA + REM DFMA.
+template <int LH, int P, int REM, bool LOADS>
+__global__ void __launch_bounds__(512, 1) mixreal(double* out, int iters, double t0) {
+  __shared__ __align__(16) double sm[6000];
+  for (int i = threadIdx.x; i < 6000; i += blockDim.x) sm[i] = 1.0 + i * 1e-6;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double acc[LH][2][2], accx[LH][2][REM > 0 ? REM : 1], tl[LH];
+#pragma unroll
+  for (int i = 0; i < LH; ++i) {
+    tl[i] = t0 + i * 1e-3;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      acc[i][mt][0] = acc[i][mt][1] = 0.0;
+#pragma unroll
+      for (int c = 0; c < (REM > 0 ? REM : 1); ++c) accx[i][mt][c] = 0.0;
+    }
+  }
+  double thr[2][P], br[LH], rvr[LH][REM > 0 ? REM : 1];
+#pragma unroll
+  for (int p = 0; p < P; ++p) thr[0][p] = thr[1][p] = 0.5 + p;
+#pragma unroll
+  for (int i = 0; i < LH; ++i) {
+    br[i] = 1.0 + i;
+#pragma unroll
+    for (int c = 0; c < (REM > 0 ? REM : 1); ++c) rvr[i][c] = 0.25 + c;
+  }
+  for (int it = 0; it < iters; ++it) {
+    const int ks = it & 3;
+    double th[2][P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if (LOADS) {
+        const double2 v = *reinterpret_cast<const double2*>(sm + p * 1088 + (ks * 4 + t) * 68 + 2 * g);
+        th[0][p] = v.x;
+        th[1][p] = v.y;
+      } else {
+        th[0][p] = thr[0][p] + it * 1e-12;
+        th[1][p] = thr[1][p] + it * 1e-12;
+      }
+    }
+    const double* wrow = sm + 3264 + (ks * 4 + t) * 124;
+#pragma unroll
+    for (int i = 0; i < LH; ++i) {
+      double b, rv[REM > 0 ? REM : 1];
+      if (LOADS) {
+        b = wrow[i * 10 + g];
+        if (REM == 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(wrow + i * 10 + 8);
+          rv[0] = v2.x;
+          rv[REM > 1 ? 1 : 0] = v2.y;
+        }
+      } else {
+        b = br[i];
+#pragma unroll
+        for (int c = 0; c < REM; ++c) rv[c] = rvr[i][c];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        double av = th[mt][P - 1];
+#pragma unroll
+        for (int p = P - 2; p >= 0; --p) av = fma(av, tl[i], th[mt][p]);
+        dmma884(acc[i][mt][0], acc[i][mt][1], av, b);
+#pragma unroll
+        for (int c = 0; c < REM; ++c) accx[i][mt][c] = fma(av, rv[c], accx[i][mt][c]);
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < LH; ++i)
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt) {
+      s += acc[i][mt][0] + acc[i][mt][1];
+#pragma unroll
+      for (int c = 0; c < REM; ++c) s += accx[i][mt][c];
+    }
+  if (s == 12345.678) out[threadIdx.x] = s;
+}
+
+template <int LH, int P, int REM, bool LOADS>
+static void runreal(int sms, double* out, int threads) {
+  const int iters = 4000;
+  float ms = time_it(mixreal<LH, P, REM, LOADS>, sms, threads, out, iters);
+  char name[64];
+  snprintf(name, sizeof name, "real LH=%d P=%d REM=%d loads=%d", LH, P, REM, (int)LOADS);
+  report(name, ms, 256.0 * 2 * LH, 2.0 * LH * (P - 1 + REM), sms, threads, iters);
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out;
   cudaMalloc(&out, 1 << 20);
-  run884<6, 1, 0, 0>(sms, out, 512);  // DMMA only
-  run884<6, 3, 0, 0>(sms, out, 512);  // Horner + DMMA
-  run884<6, 3, 0, 3>(sms, out, 512);
-  run884<6, 1, 2, 0>(sms, out, 512);  // DMMA + leftover
   run884<6, 3, 2, 0>(sms, out, 512);
-  run884<6, 3, 2, 3>(sms, out, 512);
-  run884<6, 3, 2, 3>(sms, out, 256);
-  run884<12, 3, 2, 3>(sms, out, 256);
-  run884<12, 3, 2, 3>(sms, out, 384);
-  run884<8, 3, 2, 3>(sms, out, 384);
-  run884<4, 3, 2, 3>(sms, out, 512);
-  run884<6, 4, 0, 0>(sms, out, 512);   // c5: degree 3, m = 16 -> 2 DMMA per element, no leftover
-  run884<6, 4, 0, 3>(sms, out, 512);
+  runreal<3, 3, 2, false>(sms, out, 512);
+  runreal<3, 3, 2, true>(sms, out, 512);
+  runreal<6, 3, 2, true>(sms, out, 256);
+  runreal<3, 3, 2, true>(sms, out, 256);
   return 0;
 }
