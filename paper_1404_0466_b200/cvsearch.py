@@ -236,8 +236,16 @@ class CvSession:
             self._gather = lambda c: dist.gather_curves(shard, c)
 
     @property
+    def needed_blocks(self):
+        """Row blocks this device reads (all of them without a shard; a rank's own blocks when the
+        Gram blocks are exchanged)."""
+        return self.shard.needed_blocks if self.shard is not None else list(range(self.engine.k))
+
+    @property
     def h2d_bytes(self):
-        return (self.X.numel() + self.Y.numel()) * 8
+        eng = self.engine
+        rows = sum(int(eng.row_off[b + 1] - eng.row_off[b]) for b in self.needed_blocks)
+        return rows * (eng.d + eng.m) * 8
 
     @property
     def d2h_bytes(self):
@@ -247,11 +255,19 @@ class CvSession:
     def upload(self, X, Y):
         import torch
 
+        eng = self.engine
+        blocks = self.needed_blocks
+        whole = len(blocks) == eng.k
         for dst, src in ((self.X, X), (self.Y, Y)):
-            if isinstance(src, torch.Tensor):
-                dst.copy_(src.reshape(dst.shape), non_blocking=True)
-            else:
-                dst.copy_(torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64).reshape(dst.shape)))
+            if not isinstance(src, torch.Tensor):
+                src = torch.from_numpy(np.ascontiguousarray(src, dtype=np.float64))
+            src = src.reshape(dst.shape)
+            if whole:
+                dst.copy_(src, non_blocking=True)
+                continue
+            for b in blocks:  # only the rows this rank reads
+                lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
+                dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
 
     def upload_streamed(self, X, Y):
         """Copy pinned host X/Y fold block by fold block on a side stream; returns the per-block
@@ -265,16 +281,20 @@ class CvSession:
         cs.wait_stream(torch.cuda.current_stream())  # previous users of X/Y are done
         ready = {}
         with torch.cuda.stream(cs):
-            self.Y.copy_(Y.reshape(self.Y.shape), non_blocking=True)
-            order = eng.gram_blocks + [b for b in range(eng.k) if b not in eng.gram_blocks]
+            needed = self.needed_blocks
+            Yh = Y.reshape(self.Y.shape)
+            order = [b for b in eng.gram_blocks if b in needed] + [b for b in needed if b not in eng.gram_blocks]
+            for b in order:
+                lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
+                self.Y[lo:hi].copy_(Yh[lo:hi], non_blocking=True)
             for b in order:
                 lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
                 self.X[lo:hi].copy_(X[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 ready[b] = ev
-        # later stages (hold-out of local folds) read all of X: order them after the last copy
-        self._all_copied = ev
+        # later stages (hold-out of local folds) read the local folds' rows: order them after the last copy
+        self._all_copied = ev if order else None
         return ready
 
     def sweep(self, timings=None, block_ready=None):

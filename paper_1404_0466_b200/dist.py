@@ -1,8 +1,11 @@
 """Fold sharding across the GPUs of one node.
 
 One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch). Folds are
-independent until the final mean, so fold f runs on rank f % world. Two
-exchanges are real data dependencies of the path:
+independent until the final mean. When k % world == 0 rank r owns the contiguous
+folds r*k/world .. (r+1)*k/world - 1, which are also the row blocks whose Gram it
+computes, so it uploads only those rows of X (1/world of the design); otherwise
+fold f runs on rank f % world with every block replicated. Two exchanges are
+real data dependencies of the path:
 
 * Gram blocks: the training Hessian of fold f is sum_{b != f} G_b, so every
   rank needs all k fold-block Grams. When k % world == 0 each rank computes only
@@ -30,12 +33,22 @@ class Shard:
     k: int
 
     @property
-    def local_folds(self):
-        return [f for f in range(self.k) if f % self.world == self.rank]
-
-    @property
     def exchange(self):
         return self.world > 1 and self.k % self.world == 0
+
+    def owner(self, f):
+        """Rank that computes fold f: the owner of block f when blocks are exchanged (contiguous
+        runs of k / world folds, so a rank's folds are its own Gram blocks and it needs no other
+        rows of X), round-robin otherwise."""
+        return f // (self.k // self.world) if self.exchange else f % self.world
+
+    def slot(self, f):
+        """Position of fold f among its owner's local folds."""
+        return f % (self.k // self.world) if self.exchange else f // self.world
+
+    @property
+    def local_folds(self):
+        return [f for f in range(self.k) if self.owner(f) == self.rank]
 
     @property
     def gram_blocks(self):
@@ -47,13 +60,14 @@ class Shard:
         return list(range(self.rank * per, (self.rank + 1) * per))
 
     @property
+    def needed_blocks(self):
+        """Row blocks of X / Y this rank reads: its Gram blocks and its folds' validation rows."""
+        return sorted(set(self.gram_blocks) | set(self.local_folds))
+
+    @property
     def slots(self):
         """Curves gathered per rank (ranks with fewer folds pad to this)."""
         return -(-self.k // self.world)
-
-    def fold_of_slot(self, rank, slot):
-        f = rank + slot * self.world
-        return f if f < self.k else None
 
 
 def _host_staged(t, group=None):
@@ -98,9 +112,7 @@ def gather_curves(shard, curves_local, group=None):
     pad[:nf].copy_(curves_local)
     out = torch.empty((shard.world * slots, q, m), dtype=curves_local.dtype, device=curves_local.device)
     _all_gather_into(out, pad, group=group)
-    order = []
-    for f in range(shard.k):
-        order.append((f % shard.world) * slots + f // shard.world)
+    order = [shard.owner(f) * slots + shard.slot(f) for f in range(shard.k)]
     return out[torch.as_tensor(order, device=out.device)].contiguous()
 
 

@@ -83,7 +83,9 @@ def test_shard_placement():
     s = Shard(1, 4, 5)
     assert s.local_folds == [1] and not s.exchange and s.gram_blocks == list(range(5))
     s = Shard(1, 2, 8)
-    assert s.local_folds == [1, 3, 5, 7] and s.exchange and s.gram_blocks == [4, 5, 6, 7]
+    assert s.local_folds == [4, 5, 6, 7] and s.exchange and s.gram_blocks == [4, 5, 6, 7]
+    assert s.needed_blocks == [4, 5, 6, 7] and Shard(3, 8, 8).needed_blocks == [3]
+    assert Shard(1, 3, 5).needed_blocks == list(range(5))
     # world > k (c1-c3 have k = 5 on an 8-GPU node): ranks without folds compute nothing and only
     # join the curve exchange
     s = Shard(6, 8, 5)
