@@ -35,21 +35,30 @@ static int stages_fast() {
   return solve_smem_max(LC, M, P, 4) <= (size_t)maxsm ? 4 : 3;
 }
 
+// lambda groups of warps for a chunk of LC lambdas: 8 warps for small chunks (every warp has a lambda;
+// one fold per GPU, tools/solve_nf.py: 14.4 -> 12.9 ms with 2-lambda chunks; 4 warps: 13.5 ms)
+template <int LC>
+constexpr int lg_for() {
+  return LC <= 4 ? 2 : RP_SOLVE_LG;
+}
+
 template <int M, int P, int LC>
 static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st) {
+  constexpr int LG = lg_for<LC>();
   switch (stages_fast<M, P, LC>()) {
-    case 6: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, (LC <= 4 ? 6 : 4)>(a, grid, st);
-    case 4: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(a, grid, st);
-    default: return launch_solve<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(a, grid, st);
+    case 6: return launch_solve<M / 8, M % 8, P, LC, LG, (LC <= 4 ? 6 : 4)>(a, grid, st);
+    case 4: return launch_solve<M / 8, M % 8, P, LC, LG, 4>(a, grid, st);
+    default: return launch_solve<M / 8, M % 8, P, LC, LG, 3>(a, grid, st);
   }
 }
 
 template <int M, int P, int LC>
 static int clusters_fast(int cl) {
+  constexpr int LG = lg_for<LC>();
   switch (stages_fast<M, P, LC>()) {
-    case 6: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, (LC <= 4 ? 6 : 4)>(LC, M, P, cl);
-    case 4: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, 4>(LC, M, P, cl);
-    default: return solve_clusters<M / 8, M % 8, P, LC, RP_SOLVE_LG, 3>(LC, M, P, cl);
+    case 6: return solve_clusters<M / 8, M % 8, P, LC, LG, (LC <= 4 ? 6 : 4)>(LC, M, P, cl);
+    case 4: return solve_clusters<M / 8, M % 8, P, LC, LG, 4>(LC, M, P, cl);
+    default: return solve_clusters<M / 8, M % 8, P, LC, LG, 3>(LC, M, P, cl);
   }
 }
 

@@ -3,6 +3,10 @@ import os
 import sys
 
 sys.path.insert(0, ".")
+from paper_1404_0466_b200 import _lib  # noqa: E402
+
+if os.environ.get("RP_LIB"):  # A/B of library builds
+    _lib.LIB_PATH = os.path.abspath(os.environ["RP_LIB"])
 import torch  # noqa: E402
 
 from paper_1404_0466_b200 import _lib, configs, cvsearch, dist  # noqa: E402
