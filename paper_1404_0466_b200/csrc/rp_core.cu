@@ -1178,10 +1178,16 @@ static size_t holdout_rep_bytes(int64_t N, int nf) {
   return (holdout_rep_list_bytes(N, nf) + sizeof(double) * (size_t)nf * N * REP_CHUNKS + 1023) / 1024 * 1024;
 }
 
+// per-fold 128-column tiles whose solution vectors are out of the tensor-core range (Ozaki hold-out)
+static size_t holdout_mask_bytes(int64_t N, int nf) {
+  return (sizeof(int) * (size_t)nf * ((N + 127) / 128) + 1023) / 1024 * 1024;
+}
+
 size_t rp_holdout_workspace_size(int64_t n_val, int d, int q, int m, int nf) {
   const int64_t N = (int64_t)q * m;
   const bool oz = g_holdout_ozaki && oz_holdout_supported(d, N, nf);
-  return holdout_base_bytes(n_val, d, N, nf) + holdout_rep_bytes(N, nf) + (oz ? oz_holdout_workspace(d, N, nf, false) : 0);
+  return holdout_base_bytes(n_val, d, N, nf) + holdout_rep_bytes(N, nf) + holdout_mask_bytes(N, nf) +
+         (oz ? oz_holdout_workspace(d, N, nf, false) : 0);
 }
 
 int rp_holdout_direct(const double* Xval, int64_t ldx, int64_t fold_stride_rows, int64_t n_val, int d,
@@ -1236,6 +1242,8 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
   int* rep_list = rep_count + 4;
   double* rep_part = reinterpret_cast<double*>(w8 + holdout_rep_list_bytes(N, nf));
   w8 += holdout_rep_bytes(N, nf);
+  int* col_mask = reinterpret_cast<int*>(w8);
+  w8 += holdout_mask_bytes(N, nf);
   cudaError_t e = cudaMemsetAsync(rep_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return cuda_status(e, "holdout repair count");
 
@@ -1258,11 +1266,13 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
   a.tri_a = gemm_vec2(a, A_KMAJOR) ? 1 : 0;
   int rc;
   if (a.tri_a && g_holdout_ozaki && oz_holdout_supported(d, N, nf)) {
-    // T W on the int8 tensor cores (partials [f][mtiles][N]); the DMMA product behind it runs only
-    // when the range guard trips
-    rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial, w8, st);
+    // T W on the int8 tensor cores (partials [f][mtiles][N]); the DMMA product behind it runs in full
+    // when T is out of the tensor-core range, and otherwise only for the 128-column tiles holding a
+    // solution vector out of range (c5's largest lambdas: ~8% of the columns), overwriting their partials
+    rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial, w8, col_mask, st);
     if (rc) return rc;
     a.run_if_set = oz_guard_of(w8);
+    a.tile_mask = col_mask;
   } else if (!a.tri_a) {  // the full product reads both triangles: fill G_f's upper triangle first
     const int nt = (d + 31) / 32;
     const int nmat = g_stride == 0 ? 1 : nf;

@@ -45,8 +45,11 @@ struct GemmArgs {
   int ycols;
   double* partial;  // [batch][mtiles][N]
   // gated launch (the FP64 fallback of a tensor-core product): when non-null the kernel does its
-  // work only if *run_if_set != 0 (the Ozaki range guard tripped), else every CTA exits at once
+  // work only if *run_if_set != 0 (the Ozaki range guard tripped), else every CTA exits at once --
+  // unless tile_mask is given: then, with the guard clear, it computes only the column tiles whose
+  // tile_mask[batch * ntiles + tn] is nonzero (the operand columns out of the tensor-core range)
   const int* run_if_set;
+  const int* tile_mask;
 };
 
 // Number of gated FP64 fallbacks that ran (tensor-core products whose range guard tripped);
@@ -67,9 +70,11 @@ struct GemmSmem {
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI, bool VEC2>
 __global__ void __launch_bounds__(256) dgemm_kernel(GemmArgs p) {
+  bool all_tiles = true;
   if (p.run_if_set != nullptr) {
-    if (*p.run_if_set == 0) return;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
+    all_tiles = *p.run_if_set != 0;
+    if (!all_tiles && p.tile_mask == nullptr) return;
+    if (all_tiles && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
   }
   constexpr int BK = GEMM_BK;
   constexpr int MT = WM / 8, NT = WN / 8;
@@ -97,6 +102,7 @@ __global__ void __launch_bounds__(256) dgemm_kernel(GemmArgs p) {
     tm = blockIdx.x % mtiles;
     tn = blockIdx.x / mtiles;
   }
+  if (!all_tiles && p.tile_mask[(int64_t)batch * ((p.N + BN - 1) / BN) + tn] == 0) return;
   const int m0 = tm * BM, n0 = tn * BN;
   const double* A = p.A + batch * p.strideA;
   const double* B = p.B + batch * p.strideB;
@@ -346,9 +352,11 @@ RP_DEVINL void ws_ktile(double (&acc)[MT][NT][2], const double* a_s, const doubl
 
 template <int AL, int BM, int BN, int WM, int WN, int EPI>
 __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_tiles) {
+  bool all_tiles = true;
   if (p.run_if_set != nullptr) {
-    if (*p.run_if_set == 0) return;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
+    all_tiles = *p.run_if_set != 0;
+    if (!all_tiles && p.tile_mask == nullptr) return;
+    if (all_tiles && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&g_oz_fallbacks, 1ull);
   }
   constexpr int BK = GEMM_BK;
   constexpr int MT = WM / 8, NT = WN / 8;
@@ -366,6 +374,9 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
   const int mtiles = (p.M + BM - 1) / BM, ntiles = (p.N + BN - 1) / BN;
   const int ktiles_all = (p.K + BK - 1) / BK;
   const int nbatch = total_tiles / (p.lower_only ? mtiles * (mtiles + 1) / 2 : mtiles * ntiles);
+  auto skip = [&](const TileCoord& c) {  // tiles outside the mask of a partial fallback
+    return !all_tiles && p.tile_mask[(int64_t)c.batch * ntiles + c.tn] == 0;
+  };
   auto ktiles_of = [&](int tm) {
     if (EPI != EPI_DOTB || !p.tri_a) return ktiles_all;
     const int kt = ((tm + 1) * BM + BK - 1) / BK;
@@ -386,6 +397,7 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
     int it = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
       const TileCoord tc = ws_tile(p, tile, mtiles, ntiles, nbatch);
+      if (skip(tc)) continue;
       const int m0 = tc.tm * BM, n0 = tc.tn * BN;
       const int mv = min(BM, p.M - m0), nv = min(BN, p.N - n0);
       const double* A = p.A + tc.batch * p.strideA;
@@ -450,6 +462,7 @@ __global__ void __launch_bounds__(288, 1) dgemm_ws_kernel(GemmArgs p, int total_
   int it = 0;
   for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
     const TileCoord tc = ws_tile(p, tile, mtiles, ntiles, nbatch);
+    if (skip(tc)) continue;
     const int m0 = tc.tm * BM, n0 = tc.tn * BN;
     const int batch = tc.batch;
     const int ktiles = ktiles_of(tc.tm);

@@ -84,7 +84,10 @@ RP_DEVINL bool oz_out_of_range(double mx, double se, double nz, int bits) {
 // NaN or infinite), and the range guard (range_bits).
 // One CTA per 32 rows: 8 warps stride over k (each warp reads 32 contiguous rows of A per k:
 // coalesced), then a max / sum-of-squares reduction over the warps in shared memory.
-__global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E, int* guard, int range_bits) {
+// row_mask (optional): out-of-range rows mark their 128-row tile in row_mask[b * mask_tiles + i / 128]
+// instead of tripping the guard (the hold-out's W^T rows: only those columns fall back to FP64).
+__global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E, int* guard, int range_bits,
+                                                        int* row_mask = nullptr, int mask_tiles = 0) {
   __shared__ double smx[8][32], sse[8][32], snz[8][32];
   __shared__ int sfin[8][32];
   const int b = blockIdx.y, lane = threadIdx.x & 31, wk = threadIdx.x >> 5;
@@ -122,7 +125,12 @@ __global__ void __launch_bounds__(256) oz_rowexp_kernel(OzIn in, int* E, int* gu
     int e = 0;
     if (mx > 0.0) frexp(mx, &e);
     E[(int64_t)b * mp + i] = (i < in.M && !finite) ? OZ_NONFINITE : e;
-    if (guard != nullptr && i < in.M && finite && oz_out_of_range(mx, se, nz, range_bits)) atomicOr(guard, 1);
+    if (guard != nullptr && i < in.M && finite && oz_out_of_range(mx, se, nz, range_bits)) {
+      if (row_mask != nullptr)
+        atomicOr(&row_mask[(int64_t)b * mask_tiles + i / 128], 1);
+      else
+        atomicOr(guard, 1);
+    }
   }
 }
 
@@ -829,9 +837,10 @@ inline bool oz_supported(int M, int64_t K, int nbatch) {
 // Exponents (+ range guard with the given bit budget) and K-major slices of a batch of column-major matrices (rows padded
 // to in.mpad()). The guard must have been cleared by the caller.
 inline int oz_prepare(const OzIn& in, int* E, int8_t* slices, int64_t kpad, int* guard, int range_bits,
-                      cudaStream_t st) {
+                      cudaStream_t st, int* row_mask = nullptr, int mask_tiles = 0) {
   const int mp = in.mpad();
-  oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E, guard, range_bits);
+  oz_rowexp_kernel<<<dim3((mp + 31) / 32, in.nbatch), 256, 0, st>>>(in, E, guard, range_bits, row_mask,
+                                                                     mask_tiles);
   RP_LAUNCH_CHECK("ozaki rowexp");
   cudaError_t e = oz_slice_launch(in, E, slices, kpad, guard, st);
   if (e != cudaSuccess) return cuda_status(e, "ozaki slice attributes");
@@ -1129,10 +1138,12 @@ inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
 }
 
 // part[b][I][n]: partials of w_n^T T_b w_n (sum over the ceil(d/128) entries). The range guard
-// covers both operands (rows of T and of W^T); when it trips the kernels exit and the caller's
-// gated FP64 fallback runs (as oz_syrk).
+// covers both operands: a row of T out of range trips it (the kernels exit and the caller's gated
+// FP64 fallback runs, as oz_syrk); a row of W^T (one solution vector) out of range only marks its
+// 128-column tile in col_mask (zeroed here; nbatch x ceil(N / 128) ints), and the caller's gated
+// FP64 product then recomputes just the marked tiles' partials after this kernel.
 inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
-                      int64_t N, int nbatch, double* part, void* work, cudaStream_t st) {
+                      int64_t N, int nbatch, double* part, void* work, int* col_mask, cudaStream_t st) {
   const bool shared = g_stride == 0;
   const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = shared ? 1 : nbatch;
@@ -1149,11 +1160,14 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   ia.tri = 1;
   OzIn ib{W, ldw, w_stride, d, (int)N, nbatch};  // W_b^T: row n, column k at W + k*ldw + n
   ib.Mpad = (int)mpb;
+  const int mask_tiles = (int)((N + 127) / 128);
   cudaError_t e = cudaMemsetAsync(guard, 0, sizeof(int), st);
+  if (e == cudaSuccess && col_mask != nullptr)
+    e = cudaMemsetAsync(col_mask, 0, sizeof(int) * (size_t)nbatch * mask_tiles, st);
   if (e != cudaSuccess) return cuda_status(e, "ozaki guard");
   int rc = oz_prepare(ia, EA, SA, kpad, guard, OZ_RANGE_BITS_DOT, st);
   if (rc) return rc;
-  rc = oz_prepare(ib, EB, SB, kpad, guard, OZ_RANGE_BITS_DOT, st);
+  rc = oz_prepare(ib, EB, SB, kpad, guard, OZ_RANGE_BITS_DOT, st, col_mask, mask_tiles);
   if (rc) return rc;
   CUtensorMap ta, tb;
   if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) ||

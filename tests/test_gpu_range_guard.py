@@ -169,3 +169,53 @@ def test_every_solve_instantiation(gpu, solve_lam, m, P, lam):
     assert not np.any(flags)
     worst = max(rel(W[j], orc.solve_interp(mod, G, l)) for j, l in enumerate(grid))
     assert worst <= 1e-10, worst
+
+
+def _holdout_gram_call(G, C, yy, X, Y, W, n_val, d, m, q, nf, dp, ldw):
+    """rp_holdout_gram on device copies (G: nf x d x d column-major blocks, C: nf x m x d, W: nf x dp x ldw)."""
+    dG, dC, dyy = _dev.to_dev(G), _dev.to_dev(C), _dev.to_dev(yy)
+    dX, dY, dW = _dev.to_dev(X), _dev.to_dev(Y), _dev.to_dev(W)
+    curves = _dev.empty((nf, q, m))
+    ws = _dev.workspace(_lib.query("rp_holdout_workspace_size", n_val, d, q, m, nf))
+    call("rp_holdout_gram", ptr(dG), d * d, ptr(dC), m * d, ptr(dyy), n_val, d, m, ptr(dW), ldw, dp * ldw, q, nf,
+         ptr(dX), d, n_val, ptr(dY), m, ptr(curves), ptr(ws), stream())
+    return curves.cpu().numpy()
+
+
+def test_holdout_out_of_range_columns_fall_back_per_tile(gpu):
+    """Solution vectors whose entries span more than the tensor-core hold-out's 24-bit budget (c5's
+    largest lambdas) are recomputed on FP64 DMMA tile by tile, the rest stay on the int8 tensor
+    cores: curves equal the all-DMMA path's, and no full fallback is counted."""
+    rng = np.random.default_rng(12)
+    nf, n_val, d, m, q = 2, 900, 256, 2, 160
+    dp, N = d, q * m
+    ldw = N
+    X = rng.standard_normal((nf * n_val, d)) * (1 + np.arange(d)) ** -0.5
+    Y = rng.standard_normal((nf * n_val, m))
+    W = np.zeros((nf, dp, ldw))
+    W[:, :d] = rng.standard_normal((nf, d, N)) * 1e-2
+    wide = [5, 6, 200, 301]  # columns whose entries span ~40 bits: tiles 0, 1 and 2 of 128 columns
+    for f in range(nf):
+        for c in wide[f:]:
+            W[f, :d, c] *= np.logspace(-12, 0, d)[rng.permutation(d)]
+    G = np.stack([np.ascontiguousarray((X[f * n_val:(f + 1) * n_val].T @ X[f * n_val:(f + 1) * n_val]).T)
+                  for f in range(nf)])
+    C = np.stack([(X[f * n_val:(f + 1) * n_val].T @ Y[f * n_val:(f + 1) * n_val]).T for f in range(nf)])
+    yy = np.stack([np.sum(Y[f * n_val:(f + 1) * n_val] ** 2, axis=0) for f in range(nf)])
+    before = fallbacks()
+    got = _holdout_gram_call(G, C, yy, X, Y, W, n_val, d, m, q, nf, dp, ldw)
+    assert fallbacks() == before  # only the marked tiles ran on DMMA, not a full fallback
+    call("rp_set_option", b"holdout_ozaki", 0)
+    try:
+        dmma = _holdout_gram_call(G, C, yy, X, Y, W, n_val, d, m, q, nf, dp, ldw)
+    finally:
+        call("rp_set_option", b"holdout_ozaki", 1)
+    ref = np.stack([[orc.holdout_error(W[f, :d, j * m:(j + 1) * m], X[f * n_val:(f + 1) * n_val],
+                                       Y[f * n_val:(f + 1) * n_val]) for j in range(q)] for f in range(nf)])
+    assert rel(dmma, ref) <= 1e-12
+    assert rel(got, ref) <= 1e-12
+    cols = np.array(wide)
+    err_wide = max(abs(got[f, c // m, c % m] - ref[f, c // m, c % m]) / ref[f, c // m, c % m]
+                   for f in range(nf) for c in cols[f:])
+    print(f"per-tile fallback: wide-column rel err {err_wide:.2e}")
+    assert err_wide <= 1e-13
