@@ -11,12 +11,19 @@ timeout 900 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline -
 # launch list of exactly one sweep, then full captures of the dominant kernels (never timed)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/${tag}_launches_c4.csv \
     python tools/one_sweep.py c4 > $o/${tag}_launch_run.log 2>&1
+# full ncu reports stay on the box (/tmp: they exceed what gpurun brings back); their summaries and
+# the per-launch DRAM traffic bench.py quotes come back as text, plus the c4 solve report
 for cfg in c4 c5; do
-  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:oz_syrk -c 1 -o $o/${tag}_${cfg}_gram -f \
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:oz_syrk -c 1 -o /tmp/${tag}_${cfg}_gram -f \
       python tools/one_sweep.py $cfg > $o/${tag}_${cfg}_ncu_gram.log 2>&1
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"eval_solve|oz_dotb" -c 3 \
-      -o $o/${tag}_${cfg}_solve -f python tools/one_sweep.py $cfg > $o/${tag}_${cfg}_ncu_solve.log 2>&1
+      -o /tmp/${tag}_${cfg}_solve -f python tools/one_sweep.py $cfg > $o/${tag}_${cfg}_ncu_solve.log 2>&1
+  python tools/ncu_summary.py /tmp/${tag}_${cfg}_gram.ncu-rep > $o/${tag}_ncu_${cfg}_gram.md 2>&1
+  python tools/ncu_summary.py /tmp/${tag}_${cfg}_solve.ncu-rep > $o/${tag}_ncu_${cfg}_solve.md 2>&1
 done
+python tools/ncu_top_json.py c4=/tmp/${tag}_c4_gram.ncu-rep c4=/tmp/${tag}_c4_solve.ncu-rep \
+    c5=/tmp/${tag}_c5_gram.ncu-rep c5=/tmp/${tag}_c5_solve.ncu-rep > $o/${tag}_ncu_top_kernels.json 2>&1
+cp /tmp/${tag}_c4_solve.ncu-rep $o/ 2>/dev/null
 tail -2 $o/${tag}_pytest_gpu.log
 python - "$tag" <<'EOF'
 import json, sys
