@@ -162,6 +162,10 @@ RP_DEVINL void tma_2d_g2s_multicast(void* dst, const CUtensorMap* map, int c0, i
       : "memory");
 }
 
+RP_DEVINL void named_bar_arrive(int id, int threads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
+}
+
 RP_DEVINL void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(threads) : "memory");
 }

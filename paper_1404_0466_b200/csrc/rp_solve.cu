@@ -137,7 +137,8 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
     // clusters only on request: measured slower at every shape tried (c4 fwd 15.6 -> 18.1 ms at 2 CTAs,
     // one fold per GPU 14.8 -> 17.7-18.4 ms at 2/4/8): the lockstep refills and the per-row cluster
     // barrier cost more than the L2/HBM reads they save (the solve is not bandwidth-bound)
-    if (g_solve_cluster > 1) plan_cluster(pl, nf, m, sms);
+    // (the small-chunk kernels run a producer warp outside the per-row cluster barrier: no clusters)
+    if (g_solve_cluster > 1 && !(pl.fast && solve_pw_lam(pl.lam))) plan_cluster(pl, nf, m, sms);
     else pl.chunks_pad = pl.chunks;
   }
   return pl;

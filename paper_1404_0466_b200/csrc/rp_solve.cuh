@@ -81,9 +81,19 @@ RP_DEVINL int tile_index(int I, int J) { return I * (I + 1) / 2 + J; }
 // Warp layout: 8 warps = 4 row groups (16 rows = 2 DMMA m-tiles each) x 2 lambda groups, so
 // every W fragment loaded from shared memory feeds two DMMAs and every coefficient fragment
 // is evaluated for half of the chunk's lambdas.
+// Small chunks (LCT <= 4: little arithmetic per slab, e.g. one fold per GPU) add a producer warp that
+// streams the slabs, so no compute warp stalls on refills (the per-slab issue cost is not hidden there).
+inline constexpr bool solve_pw_lam(int lam) { return lam > 0 && lam <= 4; }
+template <int LCT>
+constexpr bool solve_pw() {
+  return solve_pw_lam(LCT);
+}
+
 template <int NT, int REM, int PT, int LCT, int LG, int STG, bool BWD>
-__global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_constant__ SolveArgs a) {
-  constexpr int NTH = 128 * LG;  // 4 row groups x LG lambda groups of warps
+__global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
+    eval_solve_kernel(const __grid_constant__ SolveArgs a) {
+  constexpr int NTH = 128 * LG;  // 4 row groups x LG lambda groups of compute warps
+  constexpr bool PW = solve_pw<LCT>();
   constexpr int LC = LCT ? LCT : SOLVE_LC_GENERIC;
   constexpr int LH = (LC + LG - 1) / LG;
   constexpr int PM = PT ? PT : SOLVE_PMAX;
@@ -142,6 +152,10 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
   if (cl > 1) cluster_sync();  // every CTA's barriers are initialised before any remote arrival
   const uint32_t cempty0 = cl > 1 ? cluster_addr(cempty, 0) : 0;  // rank 0's cluster-release barriers
   int it0 = 0;  // slabs consumed by earlier rows (stage / phase bookkeeping)
+  auto csync = [&]() {  // barrier of the compute warps only (the producer warp never joins it)
+    if (PW) named_bar_sync(1, NTH);
+    else __syncthreads();
+  };
 
 #ifdef RP_SOLVE_PROF
   long long sp_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sp_last = clock64();
@@ -190,7 +204,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
     // slab once and multicasts it into every CTA's stage, after every warp of the cluster released that
     // stage (cempty); each CTA still copies its own W rows.
     auto issue = [&](int s) {
-      if (tid == 0 && s < nslab) {
+      if ((PW ? tid == NTH : tid == 0) && s < nslab) {
         const int it = it0 + s, st = it % STG;
         if (it >= STG) mbar_wait(&empty[st], ((it / STG) + 1) & 1);
         const int J = BWD ? (I + 1 + (s >> 2)) : (s >> 2);
@@ -228,11 +242,23 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
     // slabs in flight ahead of the consumers: 2 with the 3/4-stage rings of the large chunks (compute
     // per slab hides the copy latency), STG - 2 with the deep rings of small chunks (latency-bound)
     constexpr int AHEAD = STG >= 6 ? STG - 2 : 2;
+    if (PW && warp == NTH / 32) {
+      // producer warp: the row's slabs as far ahead as the ring allows, then wait until the compute
+      // warps are done with the row's diagonal step (it reuses the ring's memory)
+#pragma unroll 1
+      for (int s = 0; s < nslab; ++s) issue(s);
+      __syncwarp();
+      it0 += nslab;
+      if (step + 1 < a.nt) named_bar_sync(2, NTH + 32);
+      continue;
+    }
+    if (!PW) {
 #pragma unroll
-    for (int s0 = 0; s0 < AHEAD; ++s0) issue(s0);
+      for (int s0 = 0; s0 < AHEAD; ++s0) issue(s0);
+    }
 #pragma unroll 1
     for (int s = 0; s < nslab; ++s) {
-      issue(s + AHEAD);
+      if (!PW) issue(s + AHEAD);
       const int st = (it0 + s) % STG;
       mbar_wait(&full[st], ((it0 + s) / STG) & 1);
       const double* T = sT + st * stageT;
@@ -333,7 +359,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
       }
     }
     it0 += nslab;
-    __syncthreads();  // every warp is done with the ring
+    csync();  // every warp is done with the ring
     RP_SP_MARK(0);    // slabs of the row
 
     // ---- diagonal tile: stage theta_II (P x 64 x 64, forward copy) into the drained ring,
@@ -382,7 +408,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
       }
     }
     mbar_wait(&full[STG], step & 1);
-    __syncthreads();
+    csync();
     RP_SP_MARK(1);  // R = base - acc, theta_II staged
     // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows. Per 16 x 16 diagonal
     // block: evaluate it once per lambda into shared memory (with reciprocal pivots and the
@@ -411,7 +437,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
           if (!BWD && rowI + r0 + i < a.d && !(fabs(v) >= 1e-12)) a.flags[fold * a.flag_stride + l0 + l] = 1;
         }
       }
-      __syncthreads();
+      csync();
       RP_SP_MARK(2);  // evaluate the 16 x 16 block
       if (tid < cw) {
         const int l = tid / m;
@@ -438,7 +464,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i < 16; ++i) sR[(r0 + i) * S + tid] = x[i];
       }
-      __syncthreads();
+      csync();
       RP_SP_MARK(3);  // 16-row substitution
       // rows still to solve: after the block (fwd) / before it (bwd)
       if (q < 3 && (BWD ? (rg < sb) : (rg > sb))) {
@@ -512,7 +538,7 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
           }
         }
       }
-      __syncthreads();
+      csync();
       RP_SP_MARK(4);  // DMMA update of the rows below
     }
     // publish row I: private rows (read back by later slabs through the async proxy) and, for
@@ -530,10 +556,11 @@ __global__ void __launch_bounds__(128 * LG, 1) eval_solve_kernel(const __grid_co
       }
     }
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
-    __syncthreads();
+    csync();
     // the diagonal step used the ring's memory: rank 0 multicasts the next row's slabs only after every
     // CTA of the cluster is done with it
     if (cl > 1) cluster_sync();
+    if (PW && step + 1 < a.nt) named_bar_arrive(2, NTH + 32);  // the producer may refill the ring
     RP_SP_MARK(5);  // publish
   }
 #ifdef RP_SOLVE_PROF
@@ -603,13 +630,13 @@ int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
   }
   {
     ProfScope prof("eval_solve_fwd", st);
-    cudaError_t e = launch_clustered(kf, grid, 128 * LG, sf, a.cl, st, a);
+    cudaError_t e = launch_clustered(kf, grid, 128 * LG + (solve_pw<LCT>() ? 32 : 0), sf, a.cl, st, a);
     if (e != cudaSuccess) return cuda_status(e, "eval_solve fwd launch");
   }
   RP_LAUNCH_CHECK("eval_solve fwd");
   {
     ProfScope prof("eval_solve_bwd", st);
-    cudaError_t e = launch_clustered(kb, grid, 128 * LG, sb, a.cl, st, a);
+    cudaError_t e = launch_clustered(kb, grid, 128 * LG + (solve_pw<LCT>() ? 32 : 0), sb, a.cl, st, a);
     if (e != cudaSuccess) return cuda_status(e, "eval_solve bwd launch");
   }
   RP_LAUNCH_CHECK("eval_solve bwd");
@@ -627,7 +654,7 @@ int solve_clusters(int lam, int m, int P, int cl) {
     if (cl > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl);
-    cfg.blockDim = dim3(128 * LG);
+    cfg.blockDim = dim3(128 * LG + (solve_pw<LCT>() ? 32 : 0));
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -1,6 +1,7 @@
 // Specialised instantiations of the fused eval+solve for the output counts / degrees of the
 // BASELINE configs: m = 1 (c1), m = 10 (c2-c4, degree 2), m = 16 (c5, degree 3), each with the
-// lambda chunks the planner (rp_solve.cu) can pick. Every entry is exercised against the oracle by
+// lambda chunks the planner (rp_solve.cu) can pick (c5: 7-lambda chunks fill 3.9 waves of CTAs where
+// 8-lambda chunks leave the 4th wave 40% occupied). Every entry is exercised against the oracle by
 // tests/test_gpu_kernels.py::test_every_solve_instantiation (rp_set_option("solve_lam", n)).
 #include "rp_solve.cuh"
 
@@ -12,7 +13,7 @@ namespace rp {
 
 #define RP_FAST_LIST(X) \
   X(1, 3, 16) X(1, 3, 8) X(10, 3, 2) X(10, 3, 4) X(10, 3, 8) X(10, 3, 10) X(10, 3, 12) X(10, 3, 16) X(16, 4, 4) X(16, 4, 6) \
-      X(16, 4, 8)
+      X(16, 4, 7) X(16, 4, 8)
 
 bool has_solve_fast(int m, int P, int lam) {
 #define RP_HAS(M, PP, L) \

@@ -140,7 +140,7 @@ def test_near_exact_fit_holdout_matches_oracle(gpu, holdout):
 
 
 FAST_LIST = [(1, 3, 16), (1, 3, 8), (10, 3, 2), (10, 3, 4), (10, 3, 8), (10, 3, 10), (10, 3, 12), (10, 3, 16),
-             (16, 4, 4), (16, 4, 6), (16, 4, 8)]
+             (16, 4, 4), (16, 4, 6), (16, 4, 7), (16, 4, 8)]
 
 
 @pytest.fixture
