@@ -12,8 +12,8 @@
 namespace rp {
 
 #define RP_FAST_LIST(X) \
-  X(1, 3, 16) X(1, 3, 8) X(10, 3, 2) X(10, 3, 4) X(10, 3, 8) X(10, 3, 10) X(10, 3, 12) X(10, 3, 16) X(16, 4, 4) X(16, 4, 6) \
-      X(16, 4, 7) X(16, 4, 8)
+  X(1, 3, 16) X(1, 3, 8) X(10, 3, 2) X(10, 3, 3) X(10, 3, 4) X(10, 3, 6) X(10, 3, 8) X(10, 3, 10) X(10, 3, 12)          \
+      X(10, 3, 16) X(16, 4, 4) X(16, 4, 6) X(16, 4, 7) X(16, 4, 8)
 
 bool has_solve_fast(int m, int P, int lam) {
 #define RP_HAS(M, PP, L) \

@@ -195,15 +195,25 @@ class PicholEngine:
         call("rp_fit_tiles", ptr(self.A[i0]), self.d, self.s, i1 - i0, self.r, _lib.host_ptr(Pm), _lib.host_ptr(Vm),
              ptr(self.theta[i0]), ptr(self.resid[i0:]), ptr(self.ws_fit if ws is None else ws), stream())
 
+    def _solve_workspace(self):
+        """The solve workspace for the current plan (rp_set_option("solve_lam" / "solve_cluster") may change
+        the chunking after allocation: grow the buffer then instead of overrunning it)."""
+        need = max(_lib.query("rp_eval_solve_workspace_size", self.d, self.r, n, c1 - c0, self.q)
+                   for c0, c1 in self.groups for n in {max(self.nf - 1, 1), self.nf})
+        if need > self.ws_solve.numel():
+            self.ws_solve = self.torch.empty((need,), dtype=self.torch.uint8, device=self.device)
+        return self.ws_solve
+
     def stage_solve(self, part=None, ws=None):
         i0, i1 = part if part is not None else (0, self.nf)
+        if ws is None:
+            ws = self._solve_workspace()
         for gi, (c0, c1) in enumerate(self.groups):
             if len(self.groups) > 1:
                 self.rhs_g[gi][i0:i1].copy_(self.rhs[i0:i1, :, c0:c1])
             W = self.W[gi]
             call("rp_eval_solve", ptr(self.theta[i0]), self.d, self.r, i1 - i0, ptr(self.rhs_g[gi][i0]), c1 - c0,
-                 ptr(self.tvals), self.q, ptr(W[i0]), W.shape[2], ptr(self.flags[gi][i0:]),
-                 ptr(self.ws_solve if ws is None else ws), stream())
+                 ptr(self.tvals), self.q, ptr(W[i0]), W.shape[2], ptr(self.flags[gi][i0:]), ptr(ws), stream())
 
     def stage_holdout(self, X, Y):
         st = stream()

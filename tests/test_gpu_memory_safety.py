@@ -168,7 +168,7 @@ def solve_lam():
     call("rp_set_option", b"solve_lam", 0)
 
 
-@pytest.mark.parametrize("m,r,lams", [(10, 2, [2, 4, 8, 10, 12, 16]), (1, 2, [8, 16]), (16, 3, [4, 6, 8])])
+@pytest.mark.parametrize("m,r,lams", [(10, 2, [2, 3, 4, 6, 8, 10, 12, 16]), (1, 2, [8, 16]), (16, 3, [4, 6, 7, 8])])
 def test_eval_solve_bit_identical_across_chunkings(gpu, solve_lam, m, r, lams):
     """Every specialised chunk size and the planner's choice give bit-identical W (a race between chunks,
     ring stages or chunk-private rows would show up as a difference); the result matches the oracle; and
@@ -294,3 +294,21 @@ def test_sweeps_are_deterministic(gpu, holdout):
             outs.append((c.cpu().numpy().copy(), b.cpu().numpy().copy()))
     for c, b in outs[1:]:
         assert np.array_equal(c, outs[0][0]) and np.array_equal(b, outs[0][1])
+
+
+def test_solve_chunk_change_after_allocation(gpu, solve_lam):
+    """rp_set_option("solve_lam") after an engine was allocated needs a larger solve workspace for small
+    chunks; the engine grows it instead of letting the kernel overrun it, and the curves stay bit-identical."""
+    n, d, m, k, q, s, r = 1600, 256, 10, 4, 60, 4, 2
+    X, Y = configs.powerlaw(n, d, m, seed=6)
+    grid = orc.make_grid(1e-3, 1e1, q)
+    lams, V, _, ts, tsh, P = pichol.fit_basis(grid[orc.sample_indices(q, s)], r)
+    dX, dY, tv = _dev.to_dev(X), _dev.to_dev(Y), ts * grid + tsh
+    eng = PicholEngine([n // k] * k, d, m, q, s, r, holdout="gram")
+    base = eng.sweep(dX, dY, lams, P, V, tv)[0].cpu().numpy().copy()
+    size0 = eng.ws_solve.numel()
+    for lam in (2, 3, 12):
+        solve_lam(lam)
+        c = eng.sweep(dX, dY, lams, P, V, tv)[0].cpu().numpy()
+        assert np.array_equal(c, base), lam
+    assert eng.ws_solve.numel() >= size0

@@ -16,15 +16,15 @@ world = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 X, Y = configs.generate(cfg)
 shard = dist.Shard(0, world, cfg.k)
 shard_local = dist.Shard(0, world, cfg.k)
+for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=solve_cluster=8
+    k, v = kv.split("=")
+    _lib.call("rp_set_option", k.encode(), int(v))
 sess = cvsearch.CvSession([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, configs.grid_values(cfg), g=cfg.s, r=cfg.r)
 # emulate rank 0 of `world`: only its folds are local (all Gram blocks computed here, no exchange)
 from paper_1404_0466_b200.engine import PicholEngine  # noqa: E402
 eng = PicholEngine([cfg.n // cfg.k] * cfg.k, cfg.d, cfg.m, cfg.q, sess.lams.shape[0], cfg.r,
                    local_folds=shard.local_folds)
 sess.engine = eng
-for kv in filter(None, os.environ.get("RP_OPTS", "").split(",")):  # e.g. RP_OPTS=solve_cluster=8
-    k, v = kv.split("=")
-    _lib.call("rp_set_option", k.encode(), int(v))
 sess.upload(torch.from_numpy(X), torch.from_numpy(Y))
 for _ in range(2):
     sess.sweep()
