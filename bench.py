@@ -62,6 +62,24 @@ def parse():
     return ap.parse_args()
 
 
+def allreduce_max(x):
+    """Max over ranks (device tensor over NCCL, host tensor over gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def device_of(local):
+    """This rank's GPU. RP_BENCH_SAME_DEVICE=1 (functional test of the N > 1 code path on a one-GPU box,
+    with RP_BENCH_BACKEND=gloo: the ranks share cuda:0 and their collectives are host-staged; never
+    a timing) puts every rank on device 0."""
+    return 0 if os.environ.get("RP_BENCH_SAME_DEVICE") == "1" else local
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -349,8 +367,8 @@ def main():
         else:
             import torch
 
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
+            torch.cuda.set_device(device_of(local))
+            dist.init_process_group(os.environ.get("RP_BENCH_BACKEND", "nccl"))
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
         return
@@ -363,7 +381,7 @@ def run_ours(args, cfg, world, rank, local):
     from paper_1404_0466_b200 import _lib, configs, cvsearch, dist
     from paper_1404_0466_b200.engine import solve_bytes, sweep_flops
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(device_of(local))
     _lib.require_cuda()
     X, Y = configs.generate(cfg)
     grid = configs.grid_values(cfg)
@@ -400,9 +418,7 @@ def run_ours(args, cfg, world, rank, local):
     launches = _lib.query("rp_launch_count") - launches0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = allreduce_max(ms)
     value = cfg.k * cfg.q / (ms / 1e3)
 
     # ---- per-stage breakdown (separate pass, events between stages) and per-kernel times
@@ -438,9 +454,7 @@ def run_ours(args, cfg, world, rank, local):
         torch.cuda.synchronize()
         ms64 = f0.elapsed_time(f1) / n64
         if world > 1:
-            t = torch.tensor([ms64], device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms64 = float(t.item())
+            ms64 = allreduce_max(ms64)
         for o, (_, v) in opts.items():
             _lib.call("rp_set_option", o, v)
         fp64_only = {"value": cfg.k * cfg.q / (ms64 / 1e3), "unit": UNIT, "ms_per_step": ms64, "steps": n64,
@@ -456,9 +470,7 @@ def run_ours(args, cfg, world, rank, local):
         curves, best = sess.run(Xp, Yp)
     t_e2e = (time.perf_counter() - t0) / e2e_steps
     if world > 1:
-        t = torch.tensor([t_e2e], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_e2e = float(t.item())
+        t_e2e = allreduce_max(t_e2e)
     e2e_value = cfg.k * cfg.q / t_e2e
 
     # ---- the literal drop-in call (cvsearch.grid_search_pichol on numpy arrays, single GPU): the first call
@@ -529,11 +541,15 @@ def run_ours(args, cfg, world, rank, local):
                 "work_per_launch": kv["work"] / per, "ms_per_launch": kv["ms"] / per}
         if "fp64_equivalent_tflops" in kv:
             roof["fp64_equivalent_tflops"] = kv["fp64_equivalent_tflops"]
-    else:
+    elif stages:
         dom = max(stages, key=lambda s: stages[s]["ms"])
         roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
                 "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": None, "peak_src": pk["fp64_src"]}
-    stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9 if "solve" in stages else None
+    else:  # a rank without folds (N > k): it only joins the curve exchange
+        roof = {"bound": "tensor", "kernel": None, "achieved": 0.0, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": 0.0, "traffic": None, "peak_src": pk["fp64_src"]}
+    if "solve" in stages:
+        stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9
 
     out = {
         "metric": METRIC,
