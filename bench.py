@@ -505,8 +505,10 @@ def run_ours(args, cfg, world, rank, local):
     for name, key in stage_map.items():
         if name in stage_t:
             ts = stage_t[name]
-            stages[key] = {"ms": ts * 1e3, "tflops": flops[key] / ts / 1e12,
-                           "frac_fp64": flops[key] / ts / 1e12 / pk["fp64_tflops"]}
+            # algorithmic FP64 flops of the stage / its time: for the stages on the int8 tensor cores
+            # (Ozaki) this is an FP64-EQUIVALENT rate, and its ratio to the FP64 peak exceeds 1 by design
+            stages[key] = {"ms": ts * 1e3, "fp64_equiv_tflops": flops[key] / ts / 1e12,
+                           "ratio_to_fp64_peak": flops[key] / ts / 1e12 / pk["fp64_tflops"]}
     nf = len(shard.local_folds)
     # ---- roofline of the dominant single kernel (CUDA events on its launching stream)
     kernels = {}
@@ -543,8 +545,9 @@ def run_ours(args, cfg, world, rank, local):
             roof["fp64_equivalent_tflops"] = kv["fp64_equivalent_tflops"]
     elif stages:
         dom = max(stages, key=lambda s: stages[s]["ms"])
-        roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["tflops"], "peak": pk["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": stages[dom]["frac_fp64"], "traffic": None, "peak_src": pk["fp64_src"]}
+        roof = {"bound": "tensor", "kernel": dom, "achieved": stages[dom]["fp64_equiv_tflops"],
+                "peak": pk["fp64_tflops"], "unit": "TFLOP/s", "frac": stages[dom]["ratio_to_fp64_peak"],
+                "traffic": None, "peak_src": pk["fp64_src"]}
     else:  # a rank without folds (N > k): it only joins the curve exchange
         roof = {"bound": "tensor", "kernel": None, "achieved": 0.0, "peak": pk["fp64_tflops"], "unit": "TFLOP/s",
                 "frac": 0.0, "traffic": None, "peak_src": pk["fp64_src"]}

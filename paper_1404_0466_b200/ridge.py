@@ -73,10 +73,25 @@ def assemble(X, y):
     return RidgeProblem(X=X, y=y, H=H, g=g)
 
 
+def _device_H(p):
+    """p.H on the device, uploaded once per RidgeProblem (d x d: 134 MB at d = 4096, ~2.5 ms of PCIe per
+    upload) and reused by every solve_* call on it. The copy is re-uploaded when p.H is replaced or
+    when a sample of its entries changed in place."""
+    H = np.asarray(p.H, dtype=float)
+    flat = H.reshape(-1)
+    probe = flat[:: max(1, flat.size // 61)].copy()
+    key = (id(p.H), H.__array_interface__["data"][0], H.shape)
+    cached = getattr(p, "_H_dev", None)
+    if cached is None or cached[0] != key or not np.array_equal(cached[1], probe):
+        cached = (key, probe, _dev.to_dev(H))
+        object.__setattr__(p, "_H_dev", cached)
+    return cached[2]
+
+
 def _certify(p, lam, theta, backend):
     """Relative normal-equation residual ||H theta + lam theta - g|| / ||g|| (ridge.py:63-66)."""
     torch = _dev.torch()
-    H = _dev.to_dev(p.H)
+    H = _device_H(p)
     th = _dev.to_dev(theta)
     g = _dev.to_dev(p.g)
     res = float(torch.linalg.norm(H @ th + lam * th - g))

@@ -319,3 +319,24 @@ def test_pichol_driver_validates(gpu):  # test_cvsearch.py:210-214
     ds = cvsearch.Dataset(X, X[:, 0])
     with pytest.raises(UsageError):
         cvsearch.grid_search_pichol(ds, cvsearch.make_grid(0.01, 0.1, 3), cvsearch.make_folds(40, 2, seed=0), g=4)
+
+
+def test_certify_reuses_device_H_and_sees_changes(gpu):
+    """_certify keeps one device copy of H per RidgeProblem; replacing H or changing it in place is
+    picked up (the residual is the reference's ||H theta + lam theta - g|| / ||g||, ridge.py:63-66)."""
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((200, 40))
+    y = rng.standard_normal(200)
+    p = ridge.assemble(X, y)
+    s1 = ridge.solve_exact(p, 0.5)
+    first = p._H_dev[2]
+    s2 = ridge.solve_exact(p, 0.7)
+    assert p._H_dev[2] is first and s1.residual <= 1e-10 and s2.residual <= 1e-10
+    p.H[:] = p.H * 2.0  # in place: the cached copy is stale
+    theta = s2.theta
+    ref = np.linalg.norm(p.H @ theta + 0.7 * theta - p.g) / np.linalg.norm(p.g)
+    got = ridge._certify(p, 0.7, theta, ridge.CHOL).residual
+    assert abs(got - ref) <= 1e-12 * max(ref, 1.0)
+    p.H = p.H / 2.0  # replaced
+    got = ridge._certify(p, 0.7, theta, ridge.CHOL).residual
+    assert got <= 1e-10
