@@ -272,30 +272,80 @@ class CvSession:
     def upload_streamed(self, X, Y):
         """Copy pinned host X/Y fold block by fold block on a side stream; returns the per-block
         events the Gram stage waits on (the copy of block b+1 overlaps the Gram of block b)."""
+        return self._upload_into(self.X, self.Y, X, Y, None)
+
+    def _upload_into(self, Xd, Yd, X, Y, buffer_free):
+        """Per-block copies of pinned host X/Y into the device buffers Xd/Yd on the copy stream, after
+        `buffer_free` (an event: the last sweep that read Xd/Yd finished; None: everything enqueued so
+        far on the current stream). Returns {block: event}."""
         import torch
 
         eng = self.engine
         if self._copy_stream is None:
             self._copy_stream = torch.cuda.Stream()
         cs = self._copy_stream
-        cs.wait_stream(torch.cuda.current_stream())  # previous users of X/Y are done
+        if buffer_free is None:
+            cs.wait_stream(torch.cuda.current_stream())  # previous users of X/Y are done
+        else:
+            cs.wait_event(buffer_free)
         ready = {}
         with torch.cuda.stream(cs):
             needed = self.needed_blocks
-            Yh = Y.reshape(self.Y.shape)
+            Yh = Y.reshape(Yd.shape)
             order = [b for b in eng.gram_blocks if b in needed] + [b for b in needed if b not in eng.gram_blocks]
             for b in order:
                 lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
-                self.Y[lo:hi].copy_(Yh[lo:hi], non_blocking=True)
+                Yd[lo:hi].copy_(Yh[lo:hi], non_blocking=True)
             for b in order:
                 lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
-                self.X[lo:hi].copy_(X[lo:hi], non_blocking=True)
+                Xd[lo:hi].copy_(X[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 ready[b] = ev
-        # later stages (hold-out of local folds) read the local folds' rows: order them after the last copy
-        self._all_copied = ev if order else None
         return ready
+
+    def run_stream(self, pairs):
+        """Host in, host out for a sequence of (X, Y) pinned host tensors of this session's shapes
+        (several targets or datasets on one design shape): yields (curves, best index) per pair, in
+        order. The upload of pair i+1 goes into a second device buffer on the copy stream while pair
+        i's sweep runs, so in steady state the PCIe transfer hides behind the previous sweep; each
+        sweep's Gram still waits block by block for its own upload, and each result is read back to
+        the host before it is yielded."""
+        import torch
+
+        if not hasattr(self, "_X2"):
+            self._X2 = torch.empty_like(self.X)
+            self._Y2 = torch.empty_like(self.Y)
+        bufs = [(self.X, self.Y), (self._X2, self._Y2)]
+        free = [None, None]
+        it = iter(pairs)
+        cur = next(it, None)
+        if cur is None:
+            return
+        for t in cur:
+            if not (isinstance(t, torch.Tensor) and t.is_pinned()):
+                raise UsageError("run_stream takes pinned host torch tensors (X, Y)")
+        ready = self._upload_into(bufs[0][0], bufs[0][1], cur[0], cur[1], None)
+        i = 0
+        while cur is not None:
+            b = i % 2
+            cur_ready = ready
+            nxt = next(it, None)
+            if nxt is not None:  # overlaps the sweep below
+                ready = self._upload_into(bufs[1 - b][0], bufs[1 - b][1], nxt[0], nxt[1], free[1 - b])
+            curves, _, best = self.engine.sweep(bufs[b][0], bufs[b][1], self.lams, self.P, self.V, self.tvals,
+                                                exchange_grams=self._exchange, gather_curves=self._gather,
+                                                block_ready=cur_ready)
+            done = torch.cuda.Event()
+            done.record()
+            free[b] = done
+            bad = self.engine.check_numerics(self.lams)
+            if bad is not None:
+                f, j = bad
+                raise SingularInterpolant(f"interpolated factor is singular at lambda={self.grid[j]} (fold {f})")
+            yield curves.cpu().numpy(), best.cpu().numpy()
+            cur = nxt
+            i += 1
 
     def sweep(self, timings=None, block_ready=None):
         """Device-only sweep on the resident X/Y; returns device (curves, mean, best)."""

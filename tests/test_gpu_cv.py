@@ -253,3 +253,22 @@ def test_scaled_configs_on_every_tensor_core_path_match_oracle(gpu, name, n, d):
     ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(cfg.n, cfg.k), cfg.k, grid, g=cfg.s, r=cfg.r,
                                  folds=[0, cfg.k - 1], lam_idx=lam_idx)
     assert rel(curves[[0, cfg.k - 1]][:, lam_idx], ref["curves"]) <= 1e-8
+
+
+def test_run_stream_matches_run(gpu):
+    """CvSession.run_stream (double-buffered uploads: pair i+1 copies while pair i sweeps) yields, in
+    order, exactly what run() returns for each pair."""
+    import torch
+
+    k, n_blk, d, m, q = 4, 600, 96, 3, 17
+    grid = cvsearch.make_grid(1e-3, 1e1, q)
+    sess = cvsearch.CvSession([n_blk] * k, d, m, grid.values, g=4, r=2)
+    pairs = []
+    for seed in range(4):
+        X, Y = configs.powerlaw(n_blk * k, d, m, seed=20 + seed)
+        pairs.append((torch.from_numpy(X).pin_memory(), torch.from_numpy(Y).pin_memory()))
+    streamed = list(sess.run_stream(pairs))
+    assert len(streamed) == len(pairs)
+    for (X, Y), (c, b) in zip(pairs, streamed):
+        c_ref, b_ref = sess.run(X, Y)
+        assert np.array_equal(c, c_ref) and np.array_equal(b, b_ref)
