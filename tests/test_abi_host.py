@@ -102,6 +102,24 @@ def test_layout_bijection_and_index_of():
         lay.index_of(0, 1)
 
 
+@pytest.mark.parametrize("kind,h,h0", [("rowwise", 1, 64), ("rowwise", 100, 64), ("recursive", 257, 16),
+                                       ("recursive", 64, 64), ("tile", 130, 64)])
+def test_copy_plan_reassembles_the_permutation(kind, h, h0):
+    """copy_plan (trivec.py:100-120): slice runs of at least the threshold length plus element gathers
+    that together rebuild perm exactly, each destination covered once."""
+    lay = trivec.build_layout(kind, h, h0)
+    run_src, run_dst, run_len, gat_dst, gat_src = lay.copy_plan()
+    out = np.full(lay.length, -1, dtype=np.int64)
+    hits = np.zeros(lay.length, dtype=np.int64)
+    for s0, d0, n0 in zip(run_src, run_dst, run_len):
+        out[d0:d0 + n0] = np.arange(s0, s0 + n0)
+        hits[d0:d0 + n0] += 1
+    out[gat_dst] = gat_src
+    hits[gat_dst] += 1
+    assert np.array_equal(out, lay.perm) and np.all(hits == 1)
+    assert np.all(run_len >= trivec._RUN_THRESHOLD)
+
+
 def test_layout_validation():
     with pytest.raises(errors.UsageError):
         trivec.build_layout("diagonal", 4)
