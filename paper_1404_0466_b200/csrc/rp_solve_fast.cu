@@ -5,8 +5,11 @@
 // tests/test_gpu_kernels.py::test_every_solve_instantiation (rp_set_option("solve_lam", n)).
 #include "rp_solve.cuh"
 
+// Lambda groups of warps (each warp: 16 rows x ceil(LC / LG) lambdas). Large chunks: 12 warps (measured at
+// c4 in round 2: 30.5-30.9 ms for both passes vs 31.9-32.2 with 16 warps and 33+ with a producer warp added;
+// c5 408 vs 413 ms).
 #ifndef RP_SOLVE_LG
-#define RP_SOLVE_LG 4
+#define RP_SOLVE_LG 3
 #endif
 
 namespace rp {
@@ -23,7 +26,7 @@ bool has_solve_fast(int m, int P, int lam) {
   return false;
 }
 
-// 16 warps (4 row groups x 4 lambda groups): measured best of 8/12/16/24/32 warps at c4. Ring depth:
+// Ring depth:
 // small chunks (<= 4 lambdas: little arithmetic per slab, e.g. the one-fold-per-GPU case) are bound by
 // the copy latency and get a 6-stage ring with 4 slabs in flight when it fits; otherwise a 4-stage ring
 // (two slabs in flight) when it fits, else 3 stages.
