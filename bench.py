@@ -574,6 +574,11 @@ def run_ours(args, cfg, world, rank, local):
     if "solve" in stages:
         stages["solve"]["hbm_gbs"] = solve_bytes(nf, cfg.d, cfg.r) / (stages["solve"]["ms"] / 1e3) / 1e9
 
+    clocks = clk.summary()
+    if clocks.get("sm_mhz") and clocks.get("sm_max_mhz"):
+        # the peaks were measured at the maximum SM clock; under sw_power_cap the timed region runs lower:
+        # the dominant kernel's fraction of the peak scaled to the median SM clock it actually ran at
+        roof["frac_at_measured_clock"] = roof["frac"] * clocks["sm_max_mhz"] / clocks["sm_mhz"]
     out = {
         "metric": METRIC,
         "value": value,
@@ -591,7 +596,7 @@ def run_ours(args, cfg, world, rank, local):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": sess.h2d_bytes,
                 "d2h_bytes_per_step": sess.d2h_bytes, "ms_per_step": t_e2e * 1e3},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "fp64_only": fp64_only,
         "e2e_stream": e2e_stream,
         "dropin": dropin,
