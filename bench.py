@@ -505,15 +505,20 @@ def run_ours(args, cfg, world, rank, local):
         t0 = time.perf_counter()
         rep = cvs.grid_search_pichol(ds, grid_obj, folds, g=cfg.s, r=cfg.r)
         t_first = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        rep = cvs.grid_search_pichol(ds, grid_obj, folds, g=cfg.s, r=cfg.r)
-        t_call = time.perf_counter() - t0
+        calls = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            rep = cvs.grid_search_pichol(ds, grid_obj, folds, g=cfg.s, r=cfg.r)
+            calls.append(time.perf_counter() - t0)
+        t_call = float(np.median(calls))
         same = bool(np.array_equal(rep.best_index, best))
         cvs.clear_session_cache()
         dropin = {"value": cfg.k * cfg.q / t_call, "unit": UNIT, "call_s": t_call, "first_call_s": t_first,
                   "h2d_bytes_per_call": (X.size + Y.size) * 8, "same_selection_as_session": same,
-                  "note": "cvsearch.grid_search_pichol(Dataset(X, Y), ...) with pageable numpy X/Y, report built "
-                          "on the host; the first call allocates the cached session"}
+                  "calls_s": calls,
+                  "note": "cvsearch.grid_search_pichol(Dataset(X, Y), ...) with pageable numpy X/Y (staged through "
+                          "pinned slots by worker threads, overlapped with the Gram stage), report built on the "
+                          "host; median of 3 calls after the first, which allocates the cached session"}
 
     # ---- roofline of the dominant stage
     pk = peaks()

@@ -205,6 +205,8 @@ class CvSession:
     Gram blocks and curves over torch.distributed.
     """
 
+    STAGE_BYTES = 256 << 20  # each of the two pinned staging slots of upload_pageable
+
     def __init__(self, block_rows, d, m, grid_values, g=4, r=2, metric=RMSE, holdout="auto",
                  raw_monomials=False, shard=None):
         import torch
@@ -304,6 +306,65 @@ class CvSession:
                 ready[b] = ev
         return ready
 
+    def upload_pageable(self, X, Y):
+        """Pageable host X/Y (numpy): worker threads copy row chunks into two pinned staging slots while
+        the previous chunk's DMA runs on the copy stream (torch's own pageable copy moves ~11 GB/s; this
+        ~45 GB/s at c4, tools/pageable_upload.py). Returns {block: callable}: calling one copies that
+        block and returns its event, so the engine starts each block's upload right before its Gram and
+        the host copy of block b+1 overlaps the Gram of block b."""
+        import concurrent.futures as cf
+
+        import torch
+
+        eng = self.engine
+        X = np.ascontiguousarray(X, dtype=np.float64).reshape(tuple(self.X.shape))
+        Y = np.ascontiguousarray(Y, dtype=np.float64).reshape(tuple(self.Y.shape))
+        if self._copy_stream is None:
+            self._copy_stream = torch.cuda.Stream()
+        cs = self._copy_stream
+        cs.wait_stream(torch.cuda.current_stream())  # previous users of X/Y are done
+        d = eng.d
+        if getattr(self, "_stage", None) is None:
+            rows = max(1, min(eng.n, self.STAGE_BYTES // (8 * d)))
+            slots = [torch.empty((rows, d), dtype=torch.float64).pin_memory() for _ in range(2)]
+            self._stage = dict(rows=rows, slots=slots, views=[t.numpy() for t in slots], done=[None, None],
+                               next=0, pool=cf.ThreadPoolExecutor(max(1, min(8, os.cpu_count() or 1))),
+                               y=torch.empty(tuple(self.Y.shape), dtype=torch.float64).pin_memory())
+        stg = self._stage
+        workers = stg["pool"]._max_workers
+        np.copyto(stg["y"].numpy(), Y)
+        with torch.cuda.stream(cs):
+            self.Y.copy_(stg["y"], non_blocking=True)
+        y_done = torch.cuda.Event()
+        y_done.record(cs)
+
+        def copy_rows(lo, hi):
+            k = stg["next"]
+            stg["next"] = 1 - k
+            if stg["done"][k] is not None:
+                stg["done"][k].synchronize()  # the slot's previous DMA has read it
+            view = stg["views"][k]
+            part = -(-(hi - lo) // workers)
+            futs = [stg["pool"].submit(np.copyto, view[a - lo:min(hi, a + part) - lo], X[a:min(hi, a + part)])
+                    for a in range(lo, hi, part)]
+            for f in futs:
+                f.result()
+            with torch.cuda.stream(cs):
+                self.X[lo:hi].copy_(stg["slots"][k][:hi - lo], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+            stg["done"][k] = ev
+            return ev
+
+        def block(b):
+            lo, hi = int(eng.row_off[b]), int(eng.row_off[b + 1])
+            ev = y_done
+            for a in range(lo, hi, stg["rows"]):
+                ev = copy_rows(a, min(hi, a + stg["rows"]))
+            return ev
+
+        return {b: (lambda b=b: block(b)) for b in self.needed_blocks}
+
     def run_stream(self, pairs):
         """Host in, host out for a sequence of (X, Y) pinned host tensors of this session's shapes
         (several targets or datasets on one design shape): yields (curves, best index) per pair, in
@@ -356,7 +417,8 @@ class CvSession:
     def run(self, X, Y, timings=None):
         """Host in, host out: (curves (k, q, m), best index (m,)) as numpy.
 
-        Pinned torch tensors are streamed in per fold block, overlapped with the Gram stage."""
+        Pinned torch tensors are streamed in per fold block, overlapped with the Gram stage; pageable
+        arrays go through pinned staging slots the same way (upload_pageable)."""
         import torch
 
         pinned = isinstance(X, torch.Tensor) and X.is_pinned() and isinstance(Y, torch.Tensor) and Y.is_pinned()
@@ -365,9 +427,14 @@ class CvSession:
             curves, _, best = self.engine.sweep(self.X, self.Y, self.lams, self.P, self.V, self.tvals,
                                                 exchange_grams=self._exchange, gather_curves=self._gather,
                                                 timings=timings, block_ready=ready)
-        else:
+        elif isinstance(X, torch.Tensor) or isinstance(Y, torch.Tensor):
             self.upload(X, Y)
             curves, _, best = self.sweep(timings)
+        else:
+            ready = self.upload_pageable(X, Y)
+            curves, _, best = self.engine.sweep(self.X, self.Y, self.lams, self.P, self.V, self.tvals,
+                                                exchange_grams=self._exchange, gather_curves=self._gather,
+                                                timings=timings, block_ready=ready)
         bad = self.engine.check_numerics(self.lams)
         if bad is not None:
             f, j = bad

@@ -45,6 +45,14 @@ def tile_elems(d, P):
     return int(_lib.query("rp_theta_size", d, P - 1))
 
 
+def _resolve(block_ready, b):
+    """The upload event of block b (starting a deferred upload first, see stage_gram)."""
+    ev = block_ready[b]
+    if callable(ev):
+        ev = block_ready[b] = ev()
+    return ev
+
+
 class PicholEngine:
     """Preallocated device state for ``grid_search_pichol`` on one GPU.
 
@@ -146,7 +154,9 @@ class PicholEngine:
     # ------------------------------------------------------------------ stages
     def stage_gram(self, X, Y, block_ready=None, blocks=None):
         """Gram blocks. block_ready: optional {block: cuda.Event} -- the Gram of a block then waits
-        only for that block's upload, so the host->device copy of later blocks overlaps it.
+        only for that block's upload, so the host->device copy of later blocks overlaps it. A value
+        may also be a callable that starts the block's upload and returns its event; it is called
+        (and replaced by the event) right before that block's Gram is enqueued.
         blocks: a subset of this engine's Gram blocks (default all)."""
         d, m = self.d, self.m
         st = stream()
@@ -164,7 +174,7 @@ class PicholEngine:
             cur = self.torch.cuda.current_stream()
             for b in blocks:
                 if block_ready is not None:
-                    cur.wait_event(block_ready[b])
+                    cur.wait_event(_resolve(block_ready, b))
                 off, rows = int(self.row_off[b]), self.block_rows[b]
                 call("rp_gram_blocks", ptr(X[off:]), d, rows, 1, d, ptr(Y[off:]), m, m,
                      ptr(self.G[b]), ptr(self.C[b]), ptr(self.ws_gram), st)
@@ -291,8 +301,8 @@ class PicholEngine:
             return curves_all, None, None
         self.stage_gram(X, Y, block_ready)
         if block_ready is not None:  # later stages may read any row of X / Y
-            for done in block_ready.values():
-                torch.cuda.current_stream().wait_event(done)
+            for b in list(block_ready):
+                torch.cuda.current_stream().wait_event(_resolve(block_ready, b))
         if exchange_grams is not None:
             exchange_grams(self)
         self.stage_systems(sample_lams)

@@ -195,6 +195,27 @@ def test_session_streamed_upload_matches_resident_sweep(gpu, k):
     assert rel(curves_s, ref["curves"]) <= 1e-8
 
 
+def test_pageable_staged_upload_matches_resident_sweep(gpu):
+    """CvSession.run on pageable numpy arrays copies row chunks through two pinned staging slots, each
+    block's upload started right before its Gram. With slots of 7 rows (chunks straddle the fold
+    blocks, both slots reused many times) and two different datasets back to back, the curves must be
+    bit-identical to a device-resident sweep of the same data."""
+    import torch
+
+    k, n_blk, d, m, q = 4, 300, 96, 3, 13
+    grid = cvsearch.make_grid(1e-3, 1e1, q)
+    sess = cvsearch.CvSession([n_blk] * k, d, m, grid.values, g=4, r=2)
+    sess.STAGE_BYTES = 7 * d * 8
+    for seed in (31, 32):
+        X, Y = configs.powerlaw(n_blk * k, d, m, seed=seed)
+        curves_p, best_p = sess.run(X, Y)
+        sess.upload(torch.from_numpy(X), torch.from_numpy(Y))
+        curves_r, _, best_r = sess.sweep()
+        assert np.array_equal(curves_p, curves_r.cpu().numpy()), seed
+        assert np.array_equal(best_p, best_r.cpu().numpy()), seed
+    assert sess._stage["rows"] == 7
+
+
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_rank_view_is_bit_identical_to_the_full_sweep(gpu, world):
     """Each rank of a fold-sharded run (dist.Shard) computes only its folds, and only its own
