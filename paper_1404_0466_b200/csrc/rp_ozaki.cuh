@@ -17,7 +17,7 @@
 // Kernels:
 //   oz_rowexp_kernel     E[b][i] + range guard    (one pass over A, row max and sum of squares)
 //   oz_gram_prep_*       the same for A = X_b^T, fused with C_b = X_b^T Y_b (one pass over X)
-//   oz_slice_kernel      digits, K-major int8 slices [b][p][i][kpad]
+//   oz_slice_kernel      digits, K-major int8 slices [b][p][k / 32][i][32 bytes, swizzled] (oz_slice_offset)
 //   oz_syrk_pair_kernel  persistent, warp-specialised, 2-CTA clusters (tcgen05 cta_group::2,
 //                        M = 256, N = 128, K = 32): warp 0 of each CTA issues the TMA loads
 //                        (SWIZZLE_32B boxes, its own 128 rows of A_I and 64 rows of A_J), warp 1
@@ -334,8 +334,24 @@ __global__ void oz_gram_prep_reduce_kernel(const double* Cp, const double* Mp, i
   }
 }
 
-// Digits of 128 (i) x 256 (k) of A, in four 128 x 64 sub-tiles, written K-major:
-// slices[((b*S + p)*Mpad + i)*kpad + k]. Columns past K and rows past M give zero digits. Each
+// Slice layout in global memory: the shared-memory image of the tensor-core operands. For every
+// (batch b, slice p, K block kc of 32 bytes) the Mpad rows x 32 bytes are contiguous, each row's two
+// 16-byte halves swapped where bit 2 of the row is set (the SWIZZLE_32B pattern of the K-major
+// canonical layout, 8-row atoms of 256 bytes). A 128-row operand tile of one K block is therefore one
+// contiguous 4 KB run that a TMA box copies as whole 128-byte lines; the former [row][kpad] layout with
+// 32-byte box rows kept the SM's L2 request port 95% busy (one request per 32-byte sector) and the tensor
+// pipe at 78%. Byte offset of row `row` (its physical half 0) in K block kc:
+__host__ __device__ __forceinline__ int64_t oz_slice_offset(int b, int p, int row, int64_t kc, int mp, int64_t kpad) {
+  return ((((int64_t)b * OZ_S + p) * (kpad / OZ_BK) + kc) * mp + row) * OZ_BK;
+}
+
+// 2 KB row of the tensor-map view (oz_tensor_map) where operand row row0 (a multiple of 64) of K block kc starts
+RP_DEVINL int oz_box_row(int b, int p, int row0, int kc, int mp, int nkc) {
+  return ((b * OZ_S + p) * nkc + kc) * (mp >> 6) + (row0 >> 6);
+}
+
+// Digits of 128 (i) x 256 (k) of A, in four 128 x 64 sub-tiles, written K-major in the layout above.
+// Columns past K and rows past M give zero digits. Each
 // k of a sub-tile is one 1 KB contiguous read of A (consecutive threads on consecutive rows i);
 // a thread loads its 16 values of a half sub-tile before converting any (the kernel is bound by
 // load latency otherwise).
@@ -404,9 +420,12 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
       }
     }
     __syncthreads();
+    // consecutive threads write consecutive 16-byte chunks of one (slice, K block): 128 rows x 32 bytes
+    // = 4 KB contiguous; physical half h of row ri holds K chunk h ^ ((ri >> 2) & 1) (32-byte swizzle)
     for (int it = threadIdx.x; it < OZ_S * IW * 4; it += 256) {
-      const int c = it & 3, ri = (it >> 2) & (IW - 1), p = it / (4 * IW);
+      const int h = it & 1, ri = (it >> 1) & (IW - 1), kcl = (it >> 8) & 1, p = it / (4 * IW);
       const int row = i0 + ri;
+      const int c = kcl * 2 + (h ^ ((ri >> 2) & 1));
       const int64_t k = k0 + c * 16;
       if (row >= mp || k >= kpad) continue;
       uint4 v;
@@ -414,7 +433,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
       v.y = dig[p][ri][c * 4 + 1];
       v.z = dig[p][ri][c * 4 + 2];
       v.w = dig[p][ri][c * 4 + 3];
-      *reinterpret_cast<uint4*>(slices + (((int64_t)b * OZ_S + p) * mp + row) * kpad + k) = v;
+      *reinterpret_cast<uint4*>(slices + oz_slice_offset(b, p, row, k0 / OZ_BK + kcl, mp, kpad) + h * 16) = v;
     }
     __syncthreads();
   }
@@ -673,8 +692,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
       for (int u = unit0; u < a.total_tiles; u += ustep) {
         int b, I2, J;
         oz_pair_unit(u, a.per, mt, b, I2, J);
-        const int rowA = b * OZ_S * a.Mp + (2 * I2 + (int)rank) * OZ_BM;
-        const int rowB = b * OZ_S * a.Mp + J * OZ_BM + (int)rank * 64;
+        const int rowA = (2 * I2 + (int)rank) * OZ_BM;
+        const int rowB = J * OZ_BM + (int)rank * 64;
+        const int nkc = (int)(a.kpad / OZ_BK);
         for (int pass = 1; pass >= 0; --pass) {
           const int ns = pass ? OZ_S : OZ_GP;
           for (int64_t k = 0; k < a.kpad; k += OZ_BK, ++it) {
@@ -685,8 +705,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
             uint8_t* sb = sa + OZ_S * OZ_SLICE;
             const uint32_t fb = full_leader + (uint32_t)(st * 8);
             for (int p = 0; p < ns; ++p) {
-              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, (int)k, rowA + p * a.Mp, fb);
-              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, (int)k, rowB + p * a.Mp, fb);
+              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, 0, oz_box_row(b, p, rowA, (int)(k / OZ_BK), a.Mp, nkc), fb);
+              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, 0, oz_box_row(b, p, rowB, (int)(k / OZ_BK), a.Mp, nkc), fb);
             }
           }
         }
@@ -798,17 +818,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
 
 inline PFN_cuTensorMapEncodeTiled_v12000 oz_encode_fn() { return tensor_map_encoder(); }
 
-// 2-D int8 view of the slices: inner dim kpad bytes, outer nbatch*S*M rows; SWIZZLE_32B boxes of
-// 32 x 128.
+// View of the slice area as rows of 2 KB (256 x 8-byte elements; 64 operand rows x 32 bytes of one K
+// block): an operand tile is a box of box_rows / 64 consecutive rows, copied unswizzled (the swizzle is
+// already in the layout, see oz_slice_offset). Row coordinate of (b, p, kc, row0): oz_box_row().
 inline bool oz_tensor_map(CUtensorMap* m, const int8_t* slices, int64_t kpad, int64_t nrows, int box_rows = OZ_BM) {
   auto enc = oz_encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[2] = {(cuuint64_t)kpad, (cuuint64_t)nrows};
-  cuuint64_t strides[1] = {(cuuint64_t)kpad};
-  cuuint32_t box[2] = {(cuuint32_t)OZ_BK, (cuuint32_t)box_rows};
+  const int64_t total = nrows * kpad;  // bytes (nrows = nbatch * S * Mpad, Mpad a multiple of 64)
+  cuuint64_t dims[2] = {256, (cuuint64_t)(total / 2048)};
+  cuuint64_t strides[1] = {2048};
+  cuuint32_t box[2] = {256, (cuuint32_t)(box_rows / 64)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(slices), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<int8_t*>(slices), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -830,7 +852,8 @@ inline size_t oz_workspace_bytes(int M, int64_t K, int nbatch) {
 
 // Shapes the tensor-core path takes: 128-row tiles, int32 TMA coordinates.
 inline bool oz_supported(int M, int64_t K, int nbatch) {
-  return M % OZ_BM == 0 && (int64_t)nbatch * OZ_S * oz_mp(M) < 0x7fffffff && oz_kpad(K) < 0x7fffffff &&
+  // (2 KB rows of the slice view)
+  return M % OZ_BM == 0 && (int64_t)nbatch * OZ_S * (oz_mp(M) / 64) * (oz_kpad(K) / OZ_BK) < 0x7fffffff &&
          oz_encode_fn() != nullptr;
 }
 
@@ -991,8 +1014,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
         int b, I2, J;
         decode(u, b, I2, J);
         const int ba = a.a_shared ? 0 : b;
-        const int rowA = ba * OZ_S * a.MpadA + (2 * I2 + (int)rank) * OZ_BM;
-        const int rowB = b * OZ_S * a.MpadB + J * OZ_BM + (int)rank * 64;
+        const int rowA = (2 * I2 + (int)rank) * OZ_BM;
+        const int rowB = J * OZ_BM + (int)rank * 64;
+        const int nkc = (int)(a.kpad / OZ_BK);
         const int nk = ksteps(I2);
         for (int pass = 1; pass >= 0; --pass) {
           const int ns = pass ? OZ_S : OZ_GP;
@@ -1004,8 +1028,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_SYRK_THREADS, 1)
             uint8_t* sb = sa + OZ_S * OZ_SLICE;
             const uint32_t fb = full_leader + (uint32_t)(st * 8);
             for (int p = 0; p < ns; ++p) {
-              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, kk * OZ_BK, rowA + p * a.MpadA, fb);
-              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, kk * OZ_BK, rowB + p * a.MpadB, fb);
+              oz_tma_2d_pair(sa + p * OZ_SLICE, &tmA, 0, oz_box_row(ba, p, rowA, kk, a.MpadA, nkc), fb);
+              oz_tma_2d_pair(sb + p * OZ_PSLICE_B, &tmB, 0, oz_box_row(b, p, rowB, kk, a.MpadB, nkc), fb);
             }
           }
         }
@@ -1133,7 +1157,8 @@ inline size_t oz_holdout_workspace(int d, int64_t N, int nbatch, bool a_shared) 
 
 inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
   const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM);
-  return oz_kpad(d) <= oz_kchunk(oz_kpad(d)) && (int64_t)nbatch * OZ_S * (mpa > mpb ? mpa : mpb) < 0x7fffffff &&
+  return oz_kpad(d) <= oz_kchunk(oz_kpad(d)) &&
+         (int64_t)nbatch * OZ_S * ((mpa > mpb ? mpa : mpb) / 64) * (oz_kpad(d) / OZ_BK) < 0x7fffffff &&
          oz_encode_fn() != nullptr;
 }
 
