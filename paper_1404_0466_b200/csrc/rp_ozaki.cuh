@@ -220,7 +220,7 @@ constexpr int OZ_GP_ROW = 1024 + 16;  // per stage: the X row segment, then the 
 constexpr size_t OZ_GP_SMEM = sizeof(double) * OZ_GP_STAGES * OZ_GP_ROW + 2 * OZ_GP_STAGES * sizeof(uint64_t);
 
 template <int MT>
-__global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X, int64_t ldx, int64_t rows, int d,
+__global__ void __launch_bounds__(256, 2) oz_gram_prep_bulk_kernel(const double* X, int64_t ldx, int64_t rows, int d,
                                                                 const double* Y, int64_t ldy, int m, int nchunk,
                                                                 double* Cp, double* Mp, int mp, int* E, double* C,
     int* guard) {
@@ -253,10 +253,12 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
     }
   };
   for (int s2 = 0; s2 < OZ_GP_STAGES - 1; ++s2) issue(s2);
-  double acc[4][MM], mx[4], se[4], nz[4];
+  double acc[4][MM], mx[4];
+  int se[4], nz[4];  // exponent sums and nonzero counts (exact in int: rows * 2047 < 2^31)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    mx[j] = se[j] = nz[j] = 0.0;
+    mx[j] = 0.0;
+    se[j] = nz[j] = 0;
 #pragma unroll
     for (int o = 0; o < MM; ++o) acc[j][o] = 0.0;
   }
@@ -275,8 +277,8 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
         const double av = fabs(xv);
         mx[j] = (av <= 1.79769313486231570e308) ? fmax(mx[j], av) : __longlong_as_double(0x7ff0000000000000LL);
         if (av != 0.0) {
-          se[j] += (double)oz_biased_exp(av);
-          nz[j] += 1.0;
+          se[j] += oz_biased_exp(av);
+          nz[j] += 1;
         }
 #pragma unroll
         for (int o = 0; o < MM; ++o) acc[j][o] = fma(xv, yv[o], acc[j][o]);
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
     const int i = i0 + 256 * j;
     if (nchunk == 1) {
       if (E != nullptr && i < mp) E[(int64_t)b * mp + i] = i < d ? oz_exp_code(mx[j]) : 0;
-      if (guard != nullptr && i < d && oz_out_of_range(mx[j], se[j], nz[j], OZ_RANGE_BITS)) atomicOr(guard, 1);
+      if (guard != nullptr && i < d && oz_out_of_range(mx[j], (double)se[j], (double)nz[j], OZ_RANGE_BITS)) atomicOr(guard, 1);
       if (i < d) {
 #pragma unroll
         for (int o = 0; o < MM; ++o)
@@ -298,8 +300,8 @@ __global__ void __launch_bounds__(256) oz_gram_prep_bulk_kernel(const double* X,
       }
     } else if (i < d) {
       Mp[((int64_t)b * nchunk + ch) * d + i] = mx[j];
-      Mp[((int64_t)(gridDim.z + b) * nchunk + ch) * d + i] = se[j];  // exponent sums and nonzero counts
-      Mp[((int64_t)(2 * gridDim.z + b) * nchunk + ch) * d + i] = nz[j];  // after the maxima
+      Mp[((int64_t)(gridDim.z + b) * nchunk + ch) * d + i] = (double)se[j];  // exponent sums and nonzero counts
+      Mp[((int64_t)(2 * gridDim.z + b) * nchunk + ch) * d + i] = (double)nz[j];  // after the maxima
 #pragma unroll
       for (int o = 0; o < MM; ++o)
         if (o < m) Cp[(((int64_t)b * nchunk + ch) * m + o) * d + i] = acc[j][o];
