@@ -2,6 +2,8 @@
 // chunk size) kernel instantiations. The kernel itself is in rp_solve.cuh; the specialised
 // (compile-time P and chunk) instantiations used by the BASELINE configs are in rp_solve_fast.cu.
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "rp_solve.cuh"
 #include "../../include/ridgepath_b200.h"
@@ -11,6 +13,32 @@ using namespace rp;
 namespace rp {
 int g_solve_lam = 0;      // rp_set_option("solve_lam", n): 0 = the planner's choice
 int g_solve_cluster = 0;  // rp_set_option("solve_cluster", n): 2/4/8 = theta multicast clusters; 0/1 = none
+}
+
+// One side stream (with fork / join events) per calling stream, at the caller's priority.
+static bool solve_side_stream(cudaStream_t caller, cudaStream_t* side, cudaEvent_t* fork, cudaEvent_t* join) {
+  struct Side {
+    cudaStream_t s;
+    cudaEvent_t fork, join;
+  };
+  static std::mutex mu;
+  static std::map<cudaStream_t, Side> by_caller;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = by_caller.find(caller);
+  if (it == by_caller.end()) {
+    int prio = 0;
+    cudaStreamGetPriority(caller, &prio);
+    Side sd{};
+    if (cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, prio) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) != cudaSuccess)
+      return false;
+    it = by_caller.emplace(caller, sd).first;
+  }
+  *side = it->second.s;
+  *fork = it->second.fork;
+  *join = it->second.join;
+  return true;
 }
 
 static int launch_generic(int m, const SolveArgs& a, int grid, cudaStream_t st) {
@@ -38,6 +66,13 @@ struct SolvePlan {
   int lam = 0, chunks = 0, S = 0, P = 0, nt = 0;
   int cl = 1, chunks_pad = 0;  // CTAs per cluster (theta multicast), chunks per fold padded to a multiple of cl
   bool fast = false;
+  // Split plan (lam2 > 0): the main launch covers the first chunks * lam lambdas of every fold; a tail launch
+  // of tail_ctas CTAs on the SMs the main launch leaves idle covers each fold's last lam2 lambdas (one job
+  // per fold, several jobs per CTA when there are fewer idle SMs than folds).
+  int lam2 = 0, S2 = 0, tail_ctas = 0;
+  size_t work_doubles(int nf) const {
+    return (size_t)nf * nt * 64 * ((size_t)chunks_pad * S + (lam2 ? (size_t)S2 : 0));
+  }
 };
 
 static int generic_clusters(int m, int lam, int P, int cl) {
@@ -141,6 +176,39 @@ static SolvePlan plan_solve(int d, int r, int nf, int m, int q) {
     if (g_solve_cluster > 1 && !(pl.fast && solve_pw_lam(pl.lam))) plan_cluster(pl, nf, m, sms);
     else pl.chunks_pad = pl.chunks;
   }
+  // One wave that leaves SMs idle (c4: 8 folds x 17 chunks of 12 lambdas = 136 CTAs on 148 SMs): a smaller
+  // main chunk with floor(q / lam) chunks per fold, and each fold's few remaining lambdas as a short tail job
+  // on the idle SMs (c4: 144 CTAs of 11 lambdas + 4 CTAs x 2 folds x 2 lambdas). Every CTA's chain is then
+  // shorter; a chain costs ~3.35 + lam in units of one lambda's arithmetic (c4: 2 / 4 / 12 lambdas per CTA
+  // take 10.8 / 14.7 / 30.5 ms for both passes), which is what the tail must fit under.
+  if (pl.lam > 0 && pl.fast && lam_force == 0 && g_solve_cluster <= 1 && m % 2 == 0 &&
+      (long long)nf * pl.chunks <= sms) {
+    auto cost = [](int lam) { return 3.35 + lam; };
+    double best = cost(pl.lam);
+    for (int l1 = pl.lam - 1; l1 >= 5 && l1 >= pl.lam - 3; --l1) {
+      if (!has_solve_fast(m, pl.P, l1) || solve_pw_lam(l1)) continue;
+      const int c1 = q / l1, rem = q - c1 * l1;
+      const int idle = sms - nf * c1;
+      if (c1 < 1 || rem == 0 || idle < 1) continue;
+      int l2 = 0;
+      for (int l = rem; l <= 4 && l <= q; ++l)
+        if (has_solve_fast(m, pl.P, l)) {
+          l2 = l;
+          break;
+        }
+      if (l2 == 0) continue;
+      const int tail_ctas = nf < idle ? nf : idle;
+      const int jobs = (nf + tail_ctas - 1) / tail_ctas;
+      if (jobs * cost(l2) > cost(l1) || cost(l1) >= best - 1e-9) continue;
+      best = cost(l1);
+      pl.lam = l1;
+      pl.chunks = pl.chunks_pad = c1;
+      pl.S = solve_stride(l1, m);
+      pl.lam2 = l2;
+      pl.S2 = solve_stride(l2, m);
+      pl.tail_ctas = tail_ctas;
+    }
+  }
   return pl;
 }
 
@@ -180,7 +248,7 @@ extern "C" size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int 
            rp_eval_solve_workspace_size(d, 0, nf, m, 1);
   const SolvePlan pl = plan_solve(d, r, nf, m, q);
   if (pl.lam == 0) return 0;
-  return sizeof(double) * (size_t)nf * pl.chunks_pad * (size_t)pl.nt * 64 * pl.S;
+  return sizeof(double) * pl.work_doubles(nf);
 }
 
 extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m,
@@ -262,6 +330,31 @@ static int eval_solve_planned(const double* theta, int d, int r, int nf, const d
   a.S = pl.S;
   a.Wc = (double*)work;
   const int grid = nf * a.chunks;
-  if (pl.fast) return launch_solve_fast(m, P, pl.lam, a, grid, st);
-  return launch_generic(m, a, grid, st);
+  a.chunk0 = 0;
+  a.njobs = grid;
+  if (!pl.fast) return launch_generic(m, a, grid, st);
+  if (pl.lam2 == 0) return launch_solve_fast(m, P, pl.lam, a, grid, st);
+  // split plan: the tail launch goes to a side stream first in line for the SMs the main launch leaves
+  // idle (main and tail CTAs together fit the device, so neither waits for the other)
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  RP_REQUIRE(solve_side_stream(st, &side, &fork, &join), "rp_eval_solve: side stream");
+  cudaError_t e = cudaEventRecord(fork, st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+  if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve fork");
+  int rc = launch_solve_fast(m, P, pl.lam, a, grid, st);
+  if (rc) return rc;
+  SolveArgs t = a;
+  t.lam_per_cta = pl.lam2;
+  t.S = pl.S2;
+  t.chunks = t.chunks_real = 1;
+  t.chunk0 = (q + pl.lam2 - 1) / pl.lam2 - 1;  // the fold's last chunk: lambdas q - lam2 .. q - 1
+  t.njobs = nf;
+  t.Wc = a.Wc + (size_t)grid * nt * 64 * pl.S;
+  rc = launch_solve_fast(m, P, pl.lam2, t, pl.tail_ctas, side, true);
+  if (rc) return rc;
+  e = cudaEventRecord(join, side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
+  if (e != cudaSuccess) return cuda_status(e, "rp_eval_solve join");
+  return RP_OK;
 }

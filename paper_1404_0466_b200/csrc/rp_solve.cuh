@@ -66,6 +66,8 @@ struct SolveArgs {
   int chunks_real;  // chunks that cover the grid; chunks (>= chunks_real, a multiple of cl) pads the
                     // last cluster of a fold with copies of its last chunk (bit-identical duplicate writes)
   int cl;           // CTAs per cluster: consecutive chunks of one fold; rank 0 multicasts the theta slabs
+  int chunk0;       // first chunk index of this launch (a tail launch covers only a fold's last chunk)
+  int njobs;        // (fold, chunk) chains of this launch; CTA b runs jobs b, b + gridDim.x, ... in turn
   double* Wc;      // chunk-private rows of the solution (dp x S per CTA)
   int64_t ntiles;  // 64 x 64 tiles per fold
 };
@@ -131,17 +133,8 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
   auto slab_row = [&](int mt) {
     return BWD ? rg * 16 + mt * 8 + (g >> 1) + 4 * (g & 1) : rg * 16 + 2 * g + mt;
   };
-  const int fold = blockIdx.x / a.chunks, chunk = min((int)(blockIdx.x % a.chunks), a.chunks_real - 1);
   const int cl = a.cl;
   const uint32_t rank = cl > 1 ? cluster_rank() : 0;
-  const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
-  const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
-  if (nl <= 0) return;
-  const double* theta = a.theta + fold * a.theta_fold_stride;
-  double* W = a.W + fold * a.w_fold_stride;
-  double* Wc = a.Wc + (int64_t)blockIdx.x * (a.nt * 64) * S;  // this CTA's private solve rows
-  const int cw = nl * m;  // valid chunk columns
-  const int64_t wcol0 = (int64_t)l0 * m;
   if (tid == 0) {
     for (int i = 0; i <= STG; ++i) mbar_init(&full[i], 1);
     for (int i = 0; i < STG; ++i) mbar_init(&empty[i], NTH / 32);
@@ -151,7 +144,8 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
   __syncthreads();
   if (cl > 1) cluster_sync();  // every CTA's barriers are initialised before any remote arrival
   const uint32_t cempty0 = cl > 1 ? cluster_addr(cempty, 0) : 0;  // rank 0's cluster-release barriers
-  int it0 = 0;  // slabs consumed by earlier rows (stage / phase bookkeeping)
+  int it0 = 0;      // slabs consumed by earlier rows (stage / phase bookkeeping)
+  int diag_it = 0;  // diagonal tiles staged so far (phase of full[STG])
   auto csync = [&]() {  // barrier of the compute warps only (the producer warp never joins it)
     if (PW) named_bar_sync(1, NTH);
     else __syncthreads();
@@ -166,6 +160,20 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
     s_pi[e] = (uint8_t)i;
     s_pj[e] = (uint8_t)(e - i * (i + 1) / 2);
   }
+  // A CTA runs its jobs (fold, chunk) one after the other (one job per CTA unless the launch is a tail
+  // launch with fewer CTAs than jobs); barrier phases and the ring position carry over.
+#pragma unroll 1
+  for (int job = blockIdx.x; job < a.njobs; job += gridDim.x) {
+  const bool last_job = job + (int)gridDim.x >= a.njobs;
+  const int fold = job / a.chunks, chunk = a.chunk0 + min(job % a.chunks, a.chunks_real - 1);
+  const int l0 = LCT ? min(chunk * LCT, a.q - LCT) : chunk * a.lam_per_cta;
+  const int nl = LCT ? LCT : min(a.lam_per_cta, a.q - l0);
+  if (nl <= 0) continue;  // (never: every chunk of a plan holds a lambda)
+  const double* theta = a.theta + fold * a.theta_fold_stride;
+  double* W = a.W + fold * a.w_fold_stride;
+  double* Wc = a.Wc + (int64_t)job * (a.nt * 64) * S;  // this job's private solve rows
+  const int cw = nl * m;  // valid chunk columns
+  const int64_t wcol0 = (int64_t)l0 * m;
   for (int l = tid; l < nl; l += NTH) s_tv[l] = a.tvals[l0 + l];
   double tl[LH];
 #pragma unroll
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
       for (int s = 0; s < nslab; ++s) issue(s);
       __syncwarp();
       it0 += nslab;
-      if (step + 1 < a.nt) named_bar_sync(2, NTH + 32);
+      if (step + 1 < a.nt || !last_job) named_bar_sync(2, NTH + 32);
       continue;
     }
     if (!PW) {
@@ -407,7 +415,8 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
         }
       }
     }
-    mbar_wait(&full[STG], step & 1);
+    mbar_wait(&full[STG], diag_it & 1);
+    ++diag_it;
     csync();
     RP_SP_MARK(1);  // R = base - acc, theta_II staged
     // triangular solve of the 64 x 64 diagonal tile, blocked by 16 rows. Per 16 x 16 diagonal
@@ -560,9 +569,10 @@ __global__ void __launch_bounds__(128 * LG + (solve_pw<LCT>() ? 32 : 0), 1)
     // the diagonal step used the ring's memory: rank 0 multicasts the next row's slabs only after every
     // CTA of the cluster is done with it
     if (cl > 1) cluster_sync();
-    if (PW && step + 1 < a.nt) named_bar_arrive(2, NTH + 32);  // the producer may refill the ring
+    if (PW && (step + 1 < a.nt || !last_job)) named_bar_arrive(2, NTH + 32);  // the producer may refill the ring
     RP_SP_MARK(5);  // publish
   }
+  }  // jobs
 #ifdef RP_SOLVE_PROF
   if (tid == 0 && blockIdx.x == 0)
     printf("solve %s phases (Mcycles): slabs %.3f R+stage %.3f eval %.3f subst %.3f update %.3f publish %.3f\n",
@@ -616,8 +626,9 @@ static cudaError_t launch_clustered(K kern, int grid, int threads, size_t smem, 
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// tail: the launch covers only each fold's last chunk beside a main launch (profiled under its own names)
 template <int NT, int REM, int PT, int LCT, int LG = 2, int STG = SOLVE_STAGES>
-int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
+int launch_solve(const SolveArgs& a, int grid, cudaStream_t st, bool tail = false) {
   auto kf = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, false>;
   auto kb = eval_solve_kernel<NT, REM, PT, LCT, LG, STG, true>;
   const size_t sf = solve_smem_bytes(a.lam_per_cta, a.m, a.P, STG, false);
@@ -629,13 +640,13 @@ int launch_solve(const SolveArgs& a, int grid, cudaStream_t st) {
     cudaFuncSetAttribute(kb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   }
   {
-    ProfScope prof("eval_solve_fwd", st);
+    ProfScope prof(tail ? "eval_solve_fwd_tail" : "eval_solve_fwd", st);
     cudaError_t e = launch_clustered(kf, grid, 128 * LG + (solve_pw<LCT>() ? 32 : 0), sf, a.cl, st, a);
     if (e != cudaSuccess) return cuda_status(e, "eval_solve fwd launch");
   }
   RP_LAUNCH_CHECK("eval_solve fwd");
   {
-    ProfScope prof("eval_solve_bwd", st);
+    ProfScope prof(tail ? "eval_solve_bwd_tail" : "eval_solve_bwd", st);
     cudaError_t e = launch_clustered(kb, grid, 128 * LG + (solve_pw<LCT>() ? 32 : 0), sb, a.cl, st, a);
     if (e != cudaSuccess) return cuda_status(e, "eval_solve bwd launch");
   }
@@ -674,7 +685,7 @@ int solve_clusters(int lam, int m, int P, int cl) {
 }
 
 // Fast instantiations (rp_solve_fast.cu): returns -2 when (m, P, lam) has none.
-int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st);
+int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st, bool tail = false);
 bool has_solve_fast(int m, int P, int lam);
 int solve_fast_clusters(int m, int P, int lam, int cl);  // solve_clusters of that instantiation
 

@@ -15,8 +15,8 @@
 namespace rp {
 
 #define RP_FAST_LIST(X) \
-  X(1, 3, 16) X(1, 3, 8) X(10, 3, 2) X(10, 3, 3) X(10, 3, 4) X(10, 3, 6) X(10, 3, 8) X(10, 3, 10) X(10, 3, 12)          \
-      X(10, 3, 16) X(16, 4, 4) X(16, 4, 6) X(16, 4, 7) X(16, 4, 8)
+  X(1, 3, 16) X(1, 3, 8) X(10, 3, 2) X(10, 3, 3) X(10, 3, 4) X(10, 3, 6) X(10, 3, 8) X(10, 3, 9) X(10, 3, 10) X(10, 3, 11) \
+      X(10, 3, 12) X(10, 3, 16) X(16, 4, 4) X(16, 4, 6) X(16, 4, 7) X(16, 4, 8)
 
 bool has_solve_fast(int m, int P, int lam) {
 #define RP_HAS(M, PP, L) \
@@ -47,12 +47,12 @@ constexpr int lg_for() {
 }
 
 template <int M, int P, int LC>
-static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st) {
+static int launch_fast(const SolveArgs& a, int grid, cudaStream_t st, bool tail) {
   constexpr int LG = lg_for<LC>();
   switch (stages_fast<M, P, LC>()) {
-    case 6: return launch_solve<M / 8, M % 8, P, LC, LG, (LC <= 4 ? 6 : 4)>(a, grid, st);
-    case 4: return launch_solve<M / 8, M % 8, P, LC, LG, 4>(a, grid, st);
-    default: return launch_solve<M / 8, M % 8, P, LC, LG, 3>(a, grid, st);
+    case 6: return launch_solve<M / 8, M % 8, P, LC, LG, (LC <= 4 ? 6 : 4)>(a, grid, st, tail);
+    case 4: return launch_solve<M / 8, M % 8, P, LC, LG, 4>(a, grid, st, tail);
+    default: return launch_solve<M / 8, M % 8, P, LC, LG, 3>(a, grid, st, tail);
   }
 }
 
@@ -74,9 +74,9 @@ int solve_fast_clusters(int m, int P, int lam, int cl) {
   return 0;
 }
 
-int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st) {
+int launch_solve_fast(int m, int P, int lam, const SolveArgs& a, int grid, cudaStream_t st, bool tail) {
 #define RP_LAUNCH(M, PP, L) \
-  if (m == M && P == PP && lam == L) return launch_fast<M, PP, L>(a, grid, st);
+  if (m == M && P == PP && lam == L) return launch_fast<M, PP, L>(a, grid, st, tail);
   RP_FAST_LIST(RP_LAUNCH)
 #undef RP_LAUNCH
   return -2;

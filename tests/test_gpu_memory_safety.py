@@ -168,7 +168,7 @@ def solve_lam():
     call("rp_set_option", b"solve_lam", 0)
 
 
-@pytest.mark.parametrize("m,r,lams", [(10, 2, [2, 3, 4, 6, 8, 10, 12, 16]), (1, 2, [8, 16]), (16, 3, [4, 6, 7, 8])])
+@pytest.mark.parametrize("m,r,lams", [(10, 2, [2, 3, 4, 6, 8, 9, 10, 11, 12, 16]), (1, 2, [8, 16]), (16, 3, [4, 6, 7, 8])])
 def test_eval_solve_bit_identical_across_chunkings(gpu, solve_lam, m, r, lams):
     """Every specialised chunk size and the planner's choice give bit-identical W (a race between chunks,
     ring stages or chunk-private rows would show up as a difference); the result matches the oracle; and
@@ -189,6 +189,52 @@ def test_eval_solve_bit_identical_across_chunkings(gpu, solve_lam, m, r, lams):
     for _ in range(2):
         W, _ = _guarded_solve(tiles, d, r, G, tv)
         assert np.array_equal(W, base)
+
+
+@pytest.mark.parametrize("nf,q", [(8, 200), (8, 196), (5, 103)])
+def test_eval_solve_split_plan_bit_identical(gpu, solve_lam, nf, q):
+    """One wave of CTAs that leaves SMs idle (8 folds x 17 chunks of 12 lambdas on 148 SMs) is planned as
+    a main launch of smaller chunks plus a tail launch for each fold's last lambdas on the idle SMs (a tail
+    CTA runs several folds' tails in turn). The solutions are bit-identical to single-launch chunkings,
+    match the oracle, and W, flags and the workspace (main + tail rows) stay inside their red zones."""
+    m, r, d = 10, 2, 200
+    H, lams_s, tiles1, G, ts, tsh = _solve_setup(d, r, m, seed=77)
+    torch = _dev.torch()
+    te = tile_elems(d, r + 1)
+    tiles = _dev.empty((nf * te,))
+    for f in range(nf):
+        tiles[f * te:(f + 1) * te].copy_(tiles1.reshape(-1)[:te] * (1.0 + f))
+    grid = np.logspace(-2, 0, q)
+    tv = ts * grid + tsh
+    dp = padded(d)
+    rhs = _dev.zeros((nf, dp, m))
+    rhs[:, :d].copy_(torch.from_numpy(np.ascontiguousarray(G)).unsqueeze(0))
+    ldw = q * m + 4
+
+    def run():
+        W = Guarded(nf * dp * ldw)
+        fl = Guarded(nf * q)
+        ws = guarded_ws(_lib.query("rp_eval_solve_workspace_size", d, r, nf, m, q))
+        call("rp_eval_solve", ptr(tiles), d, r, nf, ptr(rhs), m, ptr(_dev.to_dev(tv)), q, ptr(W.buf), ldw,
+             ptr(fl.buf), ptr(ws.buf), stream())
+        assert W.margins_intact() and fl.margins_intact() and ws.margins_intact()
+        assert not np.any(fl.raw[MARGIN:MARGIN + fl.n].view(torch.int32)[:nf * q].cpu().numpy())
+        Wi = W.raw[MARGIN:MARGIN + nf * dp * ldw].cpu().numpy().reshape(nf, dp, ldw)
+        assert np.all(Wi[:, :, q * m:] == SENTINEL), "padding columns of W written"
+        return W.buf.cpu().numpy().reshape(nf, dp, ldw)[:, :d, :q * m].copy()
+
+    solve_lam(0)
+    base = run()  # the planner's choice (the split plan at (8, 200) and (8, 196) on a 148-SM device)
+    mod = orc.fit(H, lams_s, r)
+    for f in (0, nf - 1):
+        Wf = base[f].reshape(d, q, m)
+        for j in (0, q // 2, q - 3, q - 2, q - 1):
+            assert rel(Wf[:, j] * (1.0 + f) ** 2, orc.solve_interp(mod, G, grid[j])) <= 1e-10
+    for lam in (12, 11, 2):
+        solve_lam(lam)
+        assert np.array_equal(run(), base), f"forced chunk {lam} differs from the planner's launch"
+    solve_lam(0)
+    assert np.array_equal(run(), base)
 
 
 @pytest.fixture

@@ -139,7 +139,8 @@ def test_near_exact_fit_holdout_matches_oracle(gpu, holdout):
     assert np.array_equal(best.cpu().numpy(), ref["best"])
 
 
-FAST_LIST = [(1, 3, 16), (1, 3, 8), (10, 3, 2), (10, 3, 3), (10, 3, 4), (10, 3, 6), (10, 3, 8), (10, 3, 10), (10, 3, 12), (10, 3, 16),
+FAST_LIST = [(1, 3, 16), (1, 3, 8), (10, 3, 2), (10, 3, 3), (10, 3, 4), (10, 3, 6), (10, 3, 8), (10, 3, 9), (10, 3, 10), (10, 3, 11), (10, 3, 12),
+             (10, 3, 16),
              (16, 4, 4), (16, 4, 6), (16, 4, 7), (16, 4, 8)]
 
 
