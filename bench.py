@@ -431,8 +431,10 @@ def run_ours(args, cfg, world, rank, local):
     _lib.query("rp_profile_ms", None)
     sess.sweep()
     kern_ms = {name: _lib.query("rp_profile_ms", name.encode())
-               for name in ("oz_syrk", "eval_solve_fwd", "eval_solve_bwd", "holdout_gemm", "oz_holdout")}
+               for name in ("oz_syrk", "eval_solve_fwd", "eval_solve_bwd", "holdout_gemm", "oz_holdout",
+                            "eval_solve_fwd_tail", "eval_solve_bwd_tail")}
     solve_split = (kern_ms.pop("eval_solve_fwd"), kern_ms.pop("eval_solve_bwd"))
+    solve_tail = (kern_ms.pop("eval_solve_fwd_tail"), kern_ms.pop("eval_solve_bwd_tail"))
     kern_ms["eval_solve"] = sum(solve_split)
     _lib.call("rp_set_option", b"profile", 0)
 
@@ -543,10 +545,23 @@ def run_ours(args, cfg, world, rank, local):
                               "peak": pk["i8_tops"], "peak_src": pk["i8_src"],
                               "fp64_equivalent_tflops": flops["gram"] / (kern_ms["oz_syrk"] / 1e3) / 1e12}
     if kern_ms["eval_solve"] > 0:
+        # the main launches' share of the solve's algorithmic work: with a split plan (rp_eval_solve_plan) each
+        # fold's last few lambdas run as a concurrent tail launch on the SMs the main launch leaves idle
+        plan = np.zeros(4, dtype=np.int32)
+        share = 0.0
+        for c0, c1 in sess.engine.groups:
+            _lib.call("rp_eval_solve_plan", cfg.d, cfg.r, max(nf, 1), c1 - c0, cfg.q, _lib.host_ptr(plan))
+            main = min(cfg.q, int(plan[0]) * int(plan[1])) if plan[2] else cfg.q
+            share += (c1 - c0) / cfg.m * main / cfg.q
         kernels["eval_solve"] = {"ms": kern_ms["eval_solve"], "fwd_ms": solve_split[0], "bwd_ms": solve_split[1],
                                  "launches": 2 * len(sess.engine.groups),
-                                 "work": flops["solve"], "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
-                                 "peak_src": pk["fp64_src"]}
+                                 "work": flops["solve"] * share, "unit": "TFLOP/s", "peak": pk["fp64_tflops"],
+                                 "peak_src": pk["fp64_src"],
+                                 "plan": {"lambdas_per_cta": int(plan[0]), "ctas_per_fold": int(plan[1]),
+                                          "tail_lambdas": int(plan[2]), "tail_ctas": int(plan[3]),
+                                          "main_share_of_work": share,
+                                          "tail_fwd_ms": solve_tail[0], "tail_bwd_ms": solve_tail[1],
+                                          "note": "tail launches run beside the main launches on idle SMs"}}
     if kern_ms["oz_holdout"] > 0:
         ops = sum(ozaki_holdout_ops(cfg, nf, c1 - c0) for c0, c1 in sess.engine.groups)
         kernels["oz_holdout"] = {"ms": kern_ms["oz_holdout"], "launches": len(sess.engine.groups), "work": ops,

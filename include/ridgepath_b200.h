@@ -154,6 +154,11 @@ size_t rp_fit_workspace_size(int d, int nf, int s, int r);
  *   Degrees up to 4 run fused; a higher degree evaluates each lambda's factor into a
  *   one-plane tile buffer in the workspace (same Horner arithmetic) and solves it. */
 size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int q);
+/* The launch plan rp_eval_solve uses for this shape on the current device (introspection for
+ * benchmarks and tests; needs a GPU): plan[0] = lambdas per CTA of the main launch, plan[1] = its
+ * chunks (CTAs) per fold, plan[2] = lambdas per job of the tail launch that covers each fold's last
+ * lambdas on the SMs the main launch leaves idle (0: no tail launch), plan[3] = its CTAs. */
+int rp_eval_solve_plan(int d, int r, int nf, int m, int q, int* plan);
 int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m, const double* tvals,
                   int q, double* W, int64_t ldw, int* flags, void* work, void* stream);
 

@@ -48,6 +48,7 @@ SIGNATURES = {
     "rp_fit_tiles": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp]),
     "rp_fit_workspace_size": (_sz, [_i, _i, _i, _i]),
     "rp_eval_solve_workspace_size": (_sz, [_i, _i, _i, _i, _i]),
+    "rp_eval_solve_plan": (_i, [_i, _i, _i, _i, _i, _vp]),
     "rp_eval_solve": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _i64, _vp, _vp, _vp]),
     "rp_eval_materialize": (_i, [_vp, _i, _i, _d, _vp, _vp]),
     "rp_theta_export": (_i, [_vp, _i, _i, _vp, _i64, _vp, _vp]),

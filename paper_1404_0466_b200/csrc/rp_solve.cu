@@ -251,6 +251,18 @@ extern "C" size_t rp_eval_solve_workspace_size(int d, int r, int nf, int m, int 
   return sizeof(double) * pl.work_doubles(nf);
 }
 
+extern "C" int rp_eval_solve_plan(int d, int r, int nf, int m, int q, int* plan) {
+  RP_REQUIRE(plan != nullptr, "rp_eval_solve_plan: plan");
+  RP_REQUIRE(d >= 1 && nf >= 1 && q >= 1 && r >= 0 && m >= 1 && m <= 16, "rp_eval_solve_plan: bad sizes");
+  const bool high = r + 1 > SOLVE_PMAX;  // per-lambda degree-0 solves
+  const SolvePlan pl = plan_solve(d, high ? 0 : r, nf, m, high ? 1 : q);
+  plan[0] = pl.lam;
+  plan[1] = pl.chunks_pad;
+  plan[2] = pl.lam2;
+  plan[3] = pl.lam2 ? pl.tail_ctas : 0;
+  return RP_OK;
+}
+
 extern "C" int rp_eval_solve(const double* theta, int d, int r, int nf, const double* rhs, int m,
                              const double* tvals, int q, double* W, int64_t ldw, int* flags, void* work,
                              void* stream) {
