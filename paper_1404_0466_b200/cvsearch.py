@@ -371,7 +371,10 @@ class CvSession:
         order. The upload of pair i+1 goes into a second device buffer on the copy stream while pair
         i's sweep runs, so in steady state the PCIe transfer hides behind the previous sweep; each
         sweep's Gram still waits block by block for its own upload, and each result is read back to
-        the host before it is yielded."""
+        the host before it is yielded. The read-back is asynchronous (pinned result buffers, one per
+        parity): pair i's result is awaited only after pair i+1's sweep has been enqueued, so the device
+        never idles while the host launches the next sweep (a failure of pair i therefore surfaces when
+        its result is yielded, after pair i+1 was started)."""
         import torch
 
         if not hasattr(self, "_X2"):
@@ -388,6 +391,7 @@ class CvSession:
                 raise UsageError("run_stream takes pinned host torch tensors (X, Y)")
         ready = self._upload_into(bufs[0][0], bufs[0][1], cur[0], cur[1], None)
         i = 0
+        pending = None
         while cur is not None:
             b = i % 2
             cur_ready = ready
@@ -400,13 +404,40 @@ class CvSession:
             done = torch.cuda.Event()
             done.record()
             free[b] = done
-            bad = self.engine.check_numerics(self.lams)
-            if bad is not None:
-                f, j = bad
-                raise SingularInterpolant(f"interpolated factor is singular at lambda={self.grid[j]} (fold {f})")
-            yield curves.cpu().numpy(), best.cpu().numpy()
+            snap = self._read_back_async(curves, best, b)
+            if pending is not None:
+                yield self._await_result(pending)
+            pending = snap
             cur = nxt
             i += 1
+        if pending is not None:
+            yield self._await_result(pending)
+
+    def _read_back_async(self, curves, best, parity):
+        """Stream-ordered copies of a sweep's results (curves, selection, Cholesky info, singular flags) into
+        this parity's pinned host buffers; returns (event, buffers)."""
+        import torch
+
+        eng = self.engine
+        if not hasattr(self, "_res"):
+            self._res = [None, None]
+        src = (curves, best, eng.info, eng.flags.amax(dim=0))
+        if self._res[parity] is None or any(h.shape != t.shape for h, t in zip(self._res[parity], src)):
+            self._res[parity] = tuple(torch.empty(tuple(t.shape), dtype=t.dtype).pin_memory() for t in src)
+        for h, t in zip(self._res[parity], src):
+            h.copy_(t, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return ev, self._res[parity]
+
+    def _await_result(self, snap):
+        ev, (curves, best, info, flags) = snap
+        ev.synchronize()
+        bad = self.engine.check_numerics(self.lams, info=info.numpy(), flags=flags.numpy())
+        if bad is not None:
+            f, j = bad
+            raise SingularInterpolant(f"interpolated factor is singular at lambda={self.grid[j]} (fold {f})")
+        return curves.numpy().copy(), best.numpy().copy()
 
     def sweep(self, timings=None, block_ready=None):
         """Device-only sweep on the resident X/Y; returns device (curves, mean, best)."""

@@ -328,9 +328,10 @@ class PicholEngine:
                 timings[n1] = timings.get(n1, 0.0) + e0.elapsed_time(e1) / 1e3
         return (curves_all, self.mean, self.best) if complete else (curves_all, None, None)
 
-    def check_numerics(self, sample_lams):
-        """Raise the reference's exceptions for device-side failures (host sync)."""
-        info = self.info.cpu().numpy()
+    def check_numerics(self, sample_lams, info=None, flags=None):
+        """Raise the reference's exceptions for device-side failures (host sync). info / flags: host copies
+        taken earlier (a pipelined caller reads them back asynchronously), default the device buffers."""
+        info = self.info.cpu().numpy() if info is None else info
         if np.any(info != 0):
             i = int(np.flatnonzero(info)[0])
             f, s = divmod(i, self.s)
@@ -338,7 +339,7 @@ class PicholEngine:
                 f"leading minor of order {int(info[i])} is not positive definite "
                 f"(fold {self.local_folds[f]}, lambda={float(sample_lams[s])})"
             )
-        flags = self.flags.amax(dim=0).cpu().numpy()
+        flags = self.flags.amax(dim=0).cpu().numpy() if flags is None else flags
         if np.any(flags != 0):
             f, j = np.argwhere(flags != 0)[0]
             return int(self.local_folds[f]), int(j)
