@@ -153,7 +153,10 @@ def ncu_traffic(stage, config):
         return None
     with open(p) as f:
         k = json.load(f).get(config, {}).get(key)
-    return None if k is None else k["dram_read_bytes"] + k["dram_write_bytes"]
+    if k is None or k.get("dram_read_bytes") is None or k.get("dram_write_bytes") is None:
+        return None
+    t = k["dram_read_bytes"] + k["dram_write_bytes"]
+    return t if t == t else None  # (NaN: ncu had no DRAM counters for that capture)
 
 
 def host_info():

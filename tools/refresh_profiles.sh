@@ -16,7 +16,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 for cfg in c4 c5; do
   timeout 1200 ncu --set full --import-source on --clock-control none -k regex:oz_syrk -c 1 -o /tmp/${tag}_${cfg}_gram -f \
       python tools/one_sweep.py $cfg > $o/${tag}_${cfg}_ncu_gram.log 2>&1
-  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"eval_solve|oz_dotb" -c 3 \
+  timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"eval_solve|oz_dotb" -c 5 \
       -o /tmp/${tag}_${cfg}_solve -f python tools/one_sweep.py $cfg > $o/${tag}_${cfg}_ncu_solve.log 2>&1
   python tools/ncu_summary.py /tmp/${tag}_${cfg}_gram.ncu-rep > $o/${tag}_ncu_${cfg}_gram.md 2>&1
   python tools/ncu_summary.py /tmp/${tag}_${cfg}_solve.ncu-rep > $o/${tag}_ncu_${cfg}_solve.md 2>&1

@@ -26,8 +26,8 @@ _lib.query("rp_profile_ms", None)
 _lib.call("rp_set_option", b"profile", 0)
 recs = [l.split() for l in open(out)]
 recs = [(n, s, float(a), float(b)) for n, s, a, b in recs]
-first_end = max(i for i, r in enumerate(recs) if r[0] in ("oz_holdout", "holdout_gemm") and i < len(recs) - 1)
-recs = recs[first_end + 1:]
+second = [i for i, r in enumerate(recs) if r[0] == recs[0][0]][1]  # the second sweep's first record
+recs = recs[second:]
 t00 = recs[0][2]
 recs = [(n, s, a - t00, b - t00) for n, s, a, b in recs]
 tot = collections.defaultdict(lambda: [0, 0.0])
