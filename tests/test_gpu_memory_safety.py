@@ -224,7 +224,15 @@ def test_eval_solve_split_plan_bit_identical(gpu, solve_lam, nf, q):
         return W.buf.cpu().numpy().reshape(nf, dp, ldw)[:, :d, :q * m].copy()
 
     solve_lam(0)
-    base = run()  # the planner's choice (the split plan at (8, 200) and (8, 196) on a 148-SM device)
+    plan = np.zeros(4, dtype=np.int32)
+    call("rp_eval_solve_plan", d, r, nf, m, q, _lib.host_ptr(plan))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert plan[0] >= 1 and plan[0] * plan[1] + plan[2] >= q  # main chunks + tail cover the grid
+    if plan[2]:  # split plan: main CTAs + tail CTAs fit the device together
+        assert nf * plan[1] + plan[3] <= sms and 1 <= plan[3] <= nf
+    if (nf, q, sms) == (8, 200, 148):
+        assert tuple(plan) == (11, 18, 2, 4), plan
+    base = run()  # the planner's choice (the split plan at (8, 200) on a 148-SM device)
     mod = orc.fit(H, lams_s, r)
     for f in (0, nf - 1):
         Wf = base[f].reshape(d, q, m)
