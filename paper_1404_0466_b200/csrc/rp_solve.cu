@@ -346,8 +346,9 @@ static int eval_solve_planned(const double* theta, int d, int r, int nf, const d
   a.njobs = grid;
   if (!pl.fast) return launch_generic(m, a, grid, st);
   if (pl.lam2 == 0) return launch_solve_fast(m, P, pl.lam, a, grid, st);
-  // split plan: the tail launch goes to a side stream first in line for the SMs the main launch leaves
-  // idle (main and tail CTAs together fit the device, so neither waits for the other)
+  // split plan: the tail launch runs on a side stream, on the SMs the main launch leaves idle (main and
+  // tail CTAs together fit the device, so neither waits for the other; each stream orders its own two
+  // passes, and the caller's stream joins the side stream at the end)
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
   RP_REQUIRE(solve_side_stream(st, &side, &fork, &join), "rp_eval_solve: side stream");
