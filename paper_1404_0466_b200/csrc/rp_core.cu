@@ -244,18 +244,26 @@ struct FitArgs {
 // the column), and the kernel is sized for 4 resident CTAs per SM so enough loads are in flight to
 // cover the HBM latency.
 constexpr int FIT_THREADS = 256;
-constexpr int FIT_PAIRS = TILE_PLANE / 2;  // 34 row pairs (64 rows + 4 padding) per column x 64 columns
+constexpr int FIT_PAIRS = TILE_PLANE / 2;
+#ifndef RP_FIT_IU
+#define RP_FIT_IU 1
+#endif
+constexpr int FIT_IU = RP_FIT_IU;  // interior tiles: columns in flight per thread  // 34 row pairs (64 rows + 4 padding) per column x 64 columns
 
 // Occupancy over unrolling (measured at c4, ms): 4 CTAs x 256 threads per SM, one pair per thread in
 // flight 0.95; 2 CTAs with 2 / 3 pairs in flight 1.22 / 1.21; 3 CTAs x 2 pairs 1.10; 5 / 6 / 8 CTAs
 // (register-capped) 1.08 / 1.17 / 1.63.
-template <int SMAX, int FIT_UNROLL = 1>
+// INTERIOR: the instantiation handles only the interior tiles (fast path) / only the others; both are launched
+// over all tiles and a CTA of the wrong kind exits at once.
+// PT > 0: compile-time plane count of the interior instantiation (0 in the general one: split = an interior
+// instantiation runs beside it and owns the interior tiles).
+template <int SMAX, int FIT_UNROLL = 1, bool INTERIOR = false, int PT = 0>
 __global__ void __launch_bounds__(FIT_THREADS, SMAX <= 8 ? 4 : 1) fit_tiles_kernel(const double* L, int d, int s, int r,
                                                                 int64_t ntiles, int64_t fold_stride, FitArgs fa,
-                                                                double* theta, double* partial) {
+                                                                double* theta, double* partial, int split) {
   const int64_t tile = blockIdx.x;
   const int f = blockIdx.y;
-  const int P = r + 1;
+  const int P = PT ? PT : r + 1;
   int I = (int)((sqrt(8.0 * tile + 1.0) - 1.0) * 0.5);
   while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
   while ((int64_t)I * (I + 1) / 2 > tile) --I;
@@ -265,7 +273,66 @@ __global__ void __launch_bounds__(FIT_THREADS, SMAX <= 8 ? 4 : 1) fit_tiles_kern
   double* out = theta + f * fold_stride + tile * P * TILE_PLANE;
   const bool vec = (d & 1) == 0 && ((uintptr_t)L & 15) == 0;  // 16-byte aligned row pairs in the factors
   double res = 0.0;
-  for (int q0 = threadIdx.x; q0 < FIT_PAIRS; q0 += FIT_THREADS * FIT_UNROLL) {
+  // Interior tiles (strictly below the diagonal, all 64 rows inside the matrix: the bulk of the triangle) take a
+  // path without per-entry predicates or index divisions: a warp owns one column per step (lane = row pair, 512
+  // contiguous bytes per factor); the 4 padding rows of every column are zeros.
+  // Same arithmetic per entry as the general path below (only the order of the residual's partial sums differs).
+  const bool interior = split && vec && I > J && (I + 1) * 64 <= d;
+  if (interior != INTERIOR) return;
+  if constexpr (INTERIOR) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* src0 = Lf + (int64_t)(J * 64) * d + I * 64 + 2 * lane;
+#pragma unroll 1
+    for (int j0 = 0; j0 < 64; j0 += FIT_IU * (FIT_THREADS / 32)) {
+      double2 T[FIT_IU][SMAX];
+#pragma unroll
+      for (int u = 0; u < FIT_IU; ++u) {
+        const double* src = src0 + (int64_t)(j0 + u * (FIT_THREADS / 32) + warp) * d;
+#pragma unroll
+        for (int si = 0; si < SMAX; ++si)
+          T[u][si] = si < s ? __ldcs(reinterpret_cast<const double2*>(src + si * n)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < FIT_IU; ++u) {
+        const int e = (j0 + u * (FIT_THREADS / 32) + warp) * TILE_LD + 2 * lane;
+        constexpr int PA = PT ? PT : 5;
+        double2 th[PA];
+#pragma unroll
+        for (int p = 0; p < PA; ++p)
+          if (p < P) {
+            double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+            for (int si = 0; si < SMAX; ++si)
+              if (si < s) {
+                v0 = fma(fa.P[p][si], T[u][si].x, v0);
+                v1 = fma(fa.P[p][si], T[u][si].y, v1);
+              }
+            th[p] = make_double2(v0, v1);
+            __stcs(reinterpret_cast<double2*>(out + p * TILE_PLANE + e), th[p]);
+          }
+#pragma unroll
+        for (int si = 0; si < SMAX; ++si)
+          if (si < s) {
+            double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+            for (int p = 0; p < PA; ++p)
+              if (p < P) {
+                v0 = fma(fa.V[si][p], th[p].x, v0);
+                v1 = fma(fa.V[si][p], th[p].y, v1);
+              }
+            const double d0 = T[u][si].x - v0, d1 = T[u][si].y - v1;
+            res = fma(d0, d0, res);
+            res = fma(d1, d1, res);
+          }
+      }
+    }
+    // padding rows 64..67 of the 64 columns: two zero pairs per column and plane
+    if (threadIdx.x < 128) {
+      const int e = (threadIdx.x >> 1) * TILE_LD + 64 + 2 * (threadIdx.x & 1);
+      for (int p = 0; p < P; ++p) __stcs(reinterpret_cast<double2*>(out + p * TILE_PLANE + e), make_double2(0.0, 0.0));
+    }
+  }
+  for (int q0 = threadIdx.x; !INTERIOR && q0 < FIT_PAIRS; q0 += FIT_THREADS * FIT_UNROLL) {
     double2 T[FIT_UNROLL][SMAX];
     int kind[FIT_UNROLL];  // 0: outside the tile, 1: both rows in the triangle, 2: mixed (edge / diagonal)
 #pragma unroll
@@ -1109,15 +1176,27 @@ int rp_fit_tiles(const double* L, int d, int s, int nf, int r, const double* P_h
       }
     const dim3 grid((unsigned)nt, nf);
     const int64_t fs = rp_theta_size(d, r);
+    // interior tiles on the predicate-free instantiation (degrees 2 and 3: the BASELINE configs), the rest
+    // (diagonal tiles, the last tile row of a padded matrix) on the general one
+    const int split = (s <= 8 && (r == 2 || r == 3)) ? 1 : 0;
+#define RP_FIT_LAUNCH(SM)                                                                                      \
+  do {                                                                                                         \
+    if (split && r == 2)                                                                                       \
+      fit_tiles_kernel<SM, 1, true, 3><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial, 1); \
+    else if (split)                                                                                            \
+      fit_tiles_kernel<SM, 1, true, 4><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial, 1); \
+    fit_tiles_kernel<SM><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial, split);          \
+  } while (0)
     if (s <= 4)
-      fit_tiles_kernel<4><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
+      RP_FIT_LAUNCH(4);
     else if (s <= 6)
-      fit_tiles_kernel<6><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
+      RP_FIT_LAUNCH(6);
     else if (s <= 8)
-      fit_tiles_kernel<8><<<grid, FIT_THREADS, 0, st>>>(L, d, s, r, nt, fs, fa, theta, partial);
+      RP_FIT_LAUNCH(8);
+#undef RP_FIT_LAUNCH
     else
       fit_tiles_kernel<32><<<dim3((unsigned)nt, nf), FIT_THREADS, 0, st>>>(L, d, s, r, nt, rp_theta_size(d, r), fa,
-                                                                            theta, partial);
+                                                                            theta, partial, 0);
   } else {
     double* Pd = partial + (size_t)nt * nf;
     double* Vd = Pd + (size_t)s * (r + 1);
