@@ -183,6 +183,51 @@ __global__ void fold_shift_kernel(const double* G, int nblocks, int d, int s, in
   }
 }
 
+// The same sums on row pairs (d even, 16-byte aligned G and A): 16-byte loads and streaming stores halve the
+// instruction count of the scalar kernel, which ncu showed issuing 71% of its cycles at 4.5 TB/s. Per entry the
+// additions are the scalar kernel's, in the same order. An odd column's diagonal entry is done by one thread
+// on its own, so nothing above the diagonal is read or written.
+template <int KB>
+__global__ void __launch_bounds__(256) fold_shift2_kernel(const double* G, int nblocks, int d, int s, int s0,
+                                                          int s_total, int nf, FoldSysArgs fa, double* A) {
+  const int j = blockIdx.x;  // column
+  const int64_t n = (int64_t)d * d;
+  const double* gj = G + (int64_t)j * d;
+  if ((j & 1) && threadIdx.x == 0) {  // the diagonal entry of an odd column
+    double g[KB];
+#pragma unroll
+    for (int b = 0; b < KB; ++b) g[b] = b < nblocks ? gj[b * n + j] : 0.0;
+    for (int f = 0; f < nf; ++f) {
+      const int hold = fa.folds[f];
+      double v = 0.0;
+#pragma unroll
+      for (int b = 0; b < KB; ++b)
+        if (b < nblocks && b != hold) v += g[b];
+      double* out = A + ((int64_t)f * s_total + s0) * n + (int64_t)j * d + j;
+      for (int si = 0; si < s; ++si) out[si * n] = v + fa.lams[si];
+    }
+  }
+  for (int i = j + (j & 1) + 2 * threadIdx.x; i < d; i += 2 * blockDim.x) {
+    double2 g[KB];
+#pragma unroll
+    for (int b = 0; b < KB; ++b)
+      g[b] = b < nblocks ? __ldcs(reinterpret_cast<const double2*>(gj + b * n + i)) : make_double2(0.0, 0.0);
+    for (int f = 0; f < nf; ++f) {
+      const int hold = fa.folds[f];
+      double2 v = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int b = 0; b < KB; ++b)
+        if (b < nblocks && b != hold) {
+          v.x += g[b].x;
+          v.y += g[b].y;
+        }
+      double* out = A + ((int64_t)f * s_total + s0) * n + (int64_t)j * d + i;
+      for (int si = 0; si < s; ++si)
+        __stcs(reinterpret_cast<double2*>(out + si * n), make_double2(i == j ? v.x + fa.lams[si] : v.x, v.y));
+    }
+  }
+}
+
 // rhs[f] = sum_{b != folds[f]} C_b (fixed order), row-major dp x m, rows >= d zero.
 __global__ void fold_rhs_kernel(const double* C, int nblocks, int d, int dp, int m, FoldSysArgs fa, double* rhs) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;  // over dp*m, row-major (i, o)
@@ -918,7 +963,12 @@ int rp_fold_systems(const double* G, const double* C, int nblocks, int d, int m,
         const int sc = s - s0 < FS_LAMS ? s - s0 : FS_LAMS;
         for (int i = 0; i < sc; ++i) fa.lams[i] = lams_host[s0 + i];
         double* Ac = A + (int64_t)f0 * s * d * d;
-        if (nblocks <= 16)
+        const bool pairs = (d & 1) == 0 && (((uintptr_t)G | (uintptr_t)Ac) & 15) == 0;
+        if (pairs && nblocks <= 8)
+          fold_shift2_kernel<8><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);
+        else if (pairs && nblocks <= 16)
+          fold_shift2_kernel<16><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);
+        else if (nblocks <= 16)
           fold_shift_kernel<16><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);
         else
           fold_shift_kernel<0><<<d, 256, 0, st>>>(G, nblocks, d, sc, s0, s, nfc, fa, Ac);

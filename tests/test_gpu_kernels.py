@@ -261,3 +261,35 @@ def test_holdout_gram_tensor_core_matches_dmma(gpu, request, n, d, m, k, q):
     assert rel(c_tc, c_dm) <= 1e-10
     ref = orc.grid_search_pichol(X, Y, configs.contiguous_assignments(n, k), k, grid, g=4, r=2)
     assert rel(c_tc, ref["curves"]) <= 1e-8
+
+
+@pytest.mark.parametrize("d", [130, 131, 256])
+@pytest.mark.parametrize("nb", [3, 8, 11])
+def test_fold_systems_fixed_order_sums(gpu, d, nb):
+    """rp_fold_systems (row-pair kernel for even d, scalar kernel for odd d): A[f][s] = sum_{b != f} G_b +
+    lam_s I over the lower triangle, bit-identical to the sequential sum in block order; nothing above the
+    diagonal is read (NaN there) or written (sentinel kept); fold -1 holds nothing out."""
+    torch = _dev.torch()
+    rng = np.random.default_rng(d * 100 + nb)
+    G = rng.standard_normal((nb, d, d))  # column-major blocks: G[b][j][i] = entry (i, j)
+    low = np.triu(np.ones((d, d), dtype=bool))  # [j][i] with i >= j: the lower triangle of a column-major matrix
+    G[:, ~low] = np.nan
+    folds = np.array(list(range(min(nb, 4))) + [-1], dtype=np.int32)
+    lams = np.array([0.25, 3.0, 1e-3])
+    nf, s = len(folds), len(lams)
+    sentinel = -7.25
+    A = torch.full((nf, s, d, d), sentinel, dtype=torch.float64, device=_dev.device())
+    dG = _dev.to_dev(G)
+    _lib.call("rp_fold_systems", _lib.ptr(dG), None, nb, d, 0, _lib.host_ptr(folds), nf, _lib.host_ptr(lams), s,
+              _lib.ptr(A), None, _lib.stream())
+    Ah = A.cpu().numpy()
+    for fi, f in enumerate(folds):
+        ref = np.zeros((d, d))
+        for b in range(nb):
+            if b != f:
+                ref = ref + np.where(low, G[b], 0.0)
+        for si, lam in enumerate(lams):
+            want = ref + lam * np.eye(d)
+            got = Ah[fi, si]
+            assert np.array_equal(got[low], want[low]), (f, si)
+            assert np.all(got[~low] == sentinel), "entries above the diagonal written"
