@@ -253,11 +253,16 @@ __global__ void __launch_bounds__(256, 2) oz_gram_prep_bulk_kernel(const double*
     }
   };
   for (int s2 = 0; s2 < OZ_GP_STAGES - 1; ++s2) issue(s2);
-  double acc[4][MM], mx[4];
-  int se[4], nz[4];  // exponent sums and nonzero counts (exact in int: rows * 2047 < 2^31)
+  // Column statistics on the entries' high words (sign cleared): their maximum carries the largest exponent
+  // (all the exponent code and the range guard use of the maximum; a NaN or infinity gives >= 0x7ff00000),
+  // integer exponent sums and nonzero counts (exact: rows * 2047 < 2^31). Integer work instead of FP64
+  // compares keeps the FP64 pipe for the X^T Y products.
+  double acc[4][MM];
+  unsigned mxh[4];
+  int se[4], nz[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    mx[j] = 0.0;
+    mxh[j] = 0u;
     se[j] = nz[j] = 0;
 #pragma unroll
     for (int o = 0; o < MM; ++o) acc[j][o] = 0.0;
@@ -274,10 +279,10 @@ __global__ void __launch_bounds__(256, 2) oz_gram_prep_bulk_kernel(const double*
     for (int j = 0; j < 4; ++j) {
       if (tid + 256 * j < width) {
         const double xv = xr[tid + 256 * j];
-        const double av = fabs(xv);
-        mx[j] = (av <= 1.79769313486231570e308) ? fmax(mx[j], av) : __longlong_as_double(0x7ff0000000000000LL);
-        if (av != 0.0) {
-          se[j] += oz_biased_exp(av);
+        const unsigned hi = (unsigned)__double2hiint(xv) & 0x7fffffffu;
+        mxh[j] = max(mxh[j], hi);
+        if ((hi | (unsigned)__double2loint(xv)) != 0u) {
+          se[j] += (int)(hi >> 20);
           nz[j] += 1;
         }
 #pragma unroll
@@ -286,6 +291,13 @@ __global__ void __launch_bounds__(256, 2) oz_gram_prep_bulk_kernel(const double*
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  double mx[4];  // the maximum as a double: +inf for a non-finite entry, else the high word with a zero low word
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    unsigned h = mxh[j] >= 0x7ff00000u ? 0x7ff00000u : mxh[j];
+    if (h == 0u && nz[j] > 0) h = 0x00080000u;  // only subnormal entries: 2^-1023 bounds them like their maximum
+    mx[j] = __hiloint2double((int)h, 0);
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
