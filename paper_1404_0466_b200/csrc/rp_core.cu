@@ -1398,7 +1398,9 @@ int rp_holdout_gram(double* Gf, int64_t g_stride, const double* Cf, int64_t c_st
     // T W on the int8 tensor cores (partials [f][mtiles][N]); the DMMA product behind it runs in full
     // when T is out of the tensor-core range, and otherwise only for the 128-column tiles holding a
     // solution vector out of range (c5's largest lambdas: ~8% of the columns), overwriting their partials
-    rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial, w8, col_mask, st);
+    SideStreams* ss = side_streams(st, 2);
+    rc = oz_holdout(Gf, g_stride, d, W, ldw, w_fold_stride, N, nf, partial, w8, col_mask, st, ss->s[0], ss->fork,
+                    ss->join[0]);
     if (rc) return rc;
     a.run_if_set = oz_guard_of(w8);
     a.tile_mask = col_mask;

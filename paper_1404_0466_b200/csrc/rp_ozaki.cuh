@@ -1181,8 +1181,11 @@ inline bool oz_holdout_supported(int d, int64_t N, int nbatch) {
 // FP64 fallback runs, as oz_syrk); a row of W^T (one solution vector) out of range only marks its
 // 128-column tile in col_mask (zeroed here; nbatch x ceil(N / 128) ints), and the caller's gated
 // FP64 product then recomputes just the marked tiles' partials after this kernel.
+// side / fork / join (optional): T's exponents and slices are prepared on the side stream beside W's on st
+// (two latency-bound passes, ~2 TB/s each alone); st waits for both before the product.
 inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W, int64_t ldw, int64_t w_stride,
-                      int64_t N, int nbatch, double* part, void* work, int* col_mask, cudaStream_t st) {
+                      int64_t N, int nbatch, double* part, void* work, int* col_mask, cudaStream_t st,
+                      cudaStream_t side = nullptr, cudaEvent_t fork = nullptr, cudaEvent_t join = nullptr) {
   const bool shared = g_stride == 0;
   const int64_t mpa = oz_rup(d, 256), mpb = oz_rup(N, OZ_BM), kpad = oz_kpad(d);
   const int na = shared ? 1 : nbatch;
@@ -1204,10 +1207,21 @@ inline int oz_holdout(const double* G, int64_t g_stride, int d, const double* W,
   if (e == cudaSuccess && col_mask != nullptr)
     e = cudaMemsetAsync(col_mask, 0, sizeof(int) * (size_t)nbatch * mask_tiles, st);
   if (e != cudaSuccess) return cuda_status(e, "ozaki guard");
-  int rc = oz_prepare(ia, EA, SA, kpad, guard, OZ_RANGE_BITS_DOT, st);
+  const bool two = side != nullptr && fork != nullptr && join != nullptr;
+  if (two) {  // the guard and mask are cleared before either preparation starts
+    e = cudaEventRecord(fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+    if (e != cudaSuccess) return cuda_status(e, "ozaki holdout fork");
+  }
+  int rc = oz_prepare(ia, EA, SA, kpad, guard, OZ_RANGE_BITS_DOT, two ? side : st);
   if (rc) return rc;
   rc = oz_prepare(ib, EB, SB, kpad, guard, OZ_RANGE_BITS_DOT, st, col_mask, mask_tiles);
   if (rc) return rc;
+  if (two) {
+    e = cudaEventRecord(join, side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, join, 0);
+    if (e != cudaSuccess) return cuda_status(e, "ozaki holdout join");
+  }
   CUtensorMap ta, tb;
   if (!oz_tensor_map(&ta, SA, kpad, (int64_t)na * OZ_S * mpa) ||
       !oz_tensor_map(&tb, SB, kpad, (int64_t)nbatch * OZ_S * mpb, 64))
