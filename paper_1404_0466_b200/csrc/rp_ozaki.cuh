@@ -390,15 +390,26 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
 #pragma unroll 1
     for (int half = 0; half < 2; ++half) {
       double xs[4][4];
+      if (!in.tri && ei != OZ_NONFINITE && k0 + 64 <= in.K) {
+        // the whole 64-deep sub-tile is inside the matrix: no per-entry predicates, one pointer walked by lda
+        const double* pk = Ab + (k0 + (kqb + 8 * half) * 4) * in.lda + i;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < 4; ++u) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const int kq = kqb + 2 * (4 * half + u);
-          const int64_t k = k0 + kq * 4 + r;
-          xs[u][r] =
-              (ei != OZ_NONFINITE && k < in.K && (!in.tri || k <= i)) ? __ldcs(Ab + k * in.lda + i) : 0.0;
+          for (int r = 0; r < 4; ++r) xs[u][r] = __ldcs(pk + r * in.lda);
+          pk += 8 * in.lda;
         }
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int kq = kqb + 2 * (4 * half + u);
+            const int64_t k = k0 + kq * 4 + r;
+            xs[u][r] =
+                (ei != OZ_NONFINITE && k < in.K && (!in.tri || k <= i)) ? __ldcs(Ab + k * in.lda + i) : 0.0;
+          }
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int kq = kqb + 2 * (4 * half + u);
@@ -406,6 +417,7 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
 #pragma unroll
         for (int p = 0; p < OZ_S; ++p) w[p] = 0u;
         if (ei != OZ_NONFINITE) {
+          uint32_t lo[4], hi[4];
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int64_t k = k0 + kq * 4 + r;
@@ -416,16 +428,22 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(OzIn in, const int* E, in
             // the digits d_1..d_6 (d in [-128, 127]) offset by 128, and uu >> 48 is the top digit
             // d_0 (|d_0| <= 65). Offsets are removed below by flipping each byte's top bit.
             const unsigned long long uu = (unsigned long long)(v + 0x808080808080LL);
-            const uint32_t lo = (uint32_t)uu, hi = (uint32_t)(uu >> 32);
-            const uint32_t sh = 8 * r;
-            w[6] |= (lo & 0xffu) << sh;
-            w[5] |= ((lo >> 8) & 0xffu) << sh;
-            w[4] |= ((lo >> 16) & 0xffu) << sh;
-            w[3] |= (lo >> 24) << sh;
-            w[2] |= (hi & 0xffu) << sh;
-            w[1] |= ((hi >> 8) & 0xffu) << sh;
-            w[0] |= ((uint32_t)((int)hi >> 16) & 0xffu) << sh;
+            lo[r] = (uint32_t)uu;
+            hi[r] = (uint32_t)(uu >> 32);
           }
+          // byte k of the four entries' words gathered into one word (digit word w[p], entry r in byte r): a
+          // 4 x 4 byte transpose by byte permutes (d_6..d_3 = bytes 0..3 of lo, d_2, d_1, d_0 = bytes 0..2 of hi)
+          const uint32_t a01 = __byte_perm(lo[0], lo[1], 0x5140), a23 = __byte_perm(lo[2], lo[3], 0x5140);
+          const uint32_t b01 = __byte_perm(lo[0], lo[1], 0x7362), b23 = __byte_perm(lo[2], lo[3], 0x7362);
+          const uint32_t c01 = __byte_perm(hi[0], hi[1], 0x5140), c23 = __byte_perm(hi[2], hi[3], 0x5140);
+          const uint32_t d01 = __byte_perm(hi[0], hi[1], 0x7362), d23 = __byte_perm(hi[2], hi[3], 0x7362);
+          w[6] = __byte_perm(a01, a23, 0x5410);
+          w[5] = __byte_perm(a01, a23, 0x7632);
+          w[4] = __byte_perm(b01, b23, 0x5410);
+          w[3] = __byte_perm(b01, b23, 0x7632);
+          w[2] = __byte_perm(c01, c23, 0x5410);
+          w[1] = __byte_perm(c01, c23, 0x7632);
+          w[0] = __byte_perm(d01, d23, 0x5410);
 #pragma unroll
           for (int p = 1; p < OZ_S; ++p) w[p] ^= 0x80808080u;
         }
