@@ -250,17 +250,27 @@ class ClockSampler:
 # ---------------------------------------------------------------- CPU oracle (reference arm + cpu_baseline)
 
 
-def cpu_sample(cfg, X, Y, fold, n_lam):
+def cpu_sample(cfg, X, Y, fold, n_lam, row_frac=1.0):
     """Time the oracle port on one fold: setup (assemble + s Choleskys + fit) and n_lam lambdas.
-    Returns (t_setup, t_per_lambda)."""
+    row_frac < 1 (bounded samples of the reference arm): the Hessian is assembled from the first row_frac of the
+    fold's training rows (at least d + 1, so the shifted systems stay positive definite) and its time -- linear in
+    the rows -- is scaled to all of them; the Choleskys, the fit and the lambdas are timed in full.
+    Returns (t_setup, t_per_lambda, t_assemble as timed, fraction of the rows used)."""
     from oracle import pichol_oracle as orc
 
     k, q = cfg.k, cfg.q
     grid = orc.make_grid(cfg.lo, cfg.hi, q)
     assign = np.arange(cfg.n) // (cfg.n // k)
     val = assign == fold
+    rows = np.flatnonzero(~val)
+    used = len(rows) if row_frac >= 1.0 else min(len(rows), max(cfg.d + 1, int(len(rows) * row_frac)))
+    frac = used / len(rows)
     t0 = time.perf_counter()
-    H, G = orc.assemble(X[~val], Y[~val])
+    if used == len(rows):
+        H, G = orc.assemble(X[~val], Y[~val])
+    else:
+        H, G = orc.assemble(X[rows[:used]], Y[rows[:used]])
+    ta = time.perf_counter()
     model = orc.fit(H, grid[orc.sample_indices(q, cfg.s)], cfg.r)
     t1 = time.perf_counter()
     lam_idx = np.linspace(0, q - 1, n_lam).round().astype(int)
@@ -268,7 +278,10 @@ def cpu_sample(cfg, X, Y, fold, n_lam):
         B = orc.solve_interp(model, G, grid[li])
         orc.holdout_error(B, X[val], Y[val])
     t2 = time.perf_counter()
-    return t1 - t0, (t2 - t1) / n_lam
+    return (ta - t0) / frac + (t1 - ta), (t2 - t1) / n_lam, ta - t0, frac
+
+
+REF_BUDGET_S = 150.0  # CPU time of the reference arm's K timed steps together
 
 
 def cpu_cores():
@@ -278,33 +291,46 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def cpu_fold_threads(cfg, X, Y, n_lam):
+def cpu_fold_round(cfg, X, Y, n_lam, row_frac=1.0):
+    """One round of the fold thread pool: all k folds concurrently, one BLAS thread each. Returns the per-fold
+    cpu_sample tuples and the round's wall time."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=min(cfg.k, cpu_cores())) as pool:
+            res = list(pool.map(lambda f: cpu_sample(cfg, X, Y, f, n_lam, row_frac), range(cfg.k)))
+        return res, time.perf_counter() - t0
+
+
+def cpu_fold_threads(cfg, X, Y, n_lam, row_frac=1.0):
     """The reference's fastest CPU mode on this host: its fold thread pool (threads=k, cvsearch.py:126-142,
     cli.py:322) with one BLAS thread per fold, each fold doing the multi-RHS work (setup + n_lam lambdas for
     all m outputs). tools/cpu_modes.py measured the alternatives on the GPU box (profiles/r02_cpu_modes_c4.json:
     all-threads BLAS with sequential folds 1.7 evals/s, the stock single-target driver per output 0.18, this
     mode 8.5). Returns (evals/s extrapolated to the k x q sweep, threads used, details)."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    from threadpoolctl import threadpool_limits
-
     cores = cpu_cores()
-    with threadpool_limits(limits=1):
-        t0 = time.perf_counter()
-        with ThreadPoolExecutor(max_workers=min(cfg.k, cores)) as pool:
-            res = list(pool.map(lambda f: cpu_sample(cfg, X, Y, f, n_lam), range(cfg.k)))
-        wall = time.perf_counter() - t0
+    res, wall = cpu_fold_round(cfg, X, Y, n_lam, row_frac)
     setup = max(r[0] for r in res)
     lam = max(r[1] for r in res)
     waves = -(-cfg.k // cores)
     value = cfg.k * cfg.q / (waves * (setup + cfg.q * lam))
-    return value, min(cfg.k, cores), {"t_setup_s_max": setup, "t_lambda_s_max": lam, "sample_wall_s": wall}
+    return value, min(cfg.k, cores), {"t_setup_s_max": setup, "t_lambda_s_max": lam, "sample_wall_s": wall,
+                                      "t_assemble_timed_s_max": max(r[2] for r in res),
+                                      "assemble_row_fraction": min(r[3] for r in res)}
 
 
-def fold_thread_sample_text(cfg, n_lam):
-    return (f"{cfg.name}: all k={cfg.k} folds concurrently on the reference's fold thread pool, 1 BLAS thread "
-            f"each; per fold assemble + {cfg.s} Choleskys + fit + {n_lam} of {cfg.q} lambdas (m={cfg.m} RHS) on the "
-            f"oracle port, extrapolated linearly to all {cfg.q} lambdas")
+def fold_thread_sample_text(cfg, n_lam, bounded=False):
+    txt = (f"{cfg.name}: all k={cfg.k} folds concurrently on the reference's fold thread pool, 1 BLAS thread "
+           f"each; per fold assemble + {cfg.s} Choleskys + fit + {n_lam} of {cfg.q} lambdas (m={cfg.m} RHS) on the "
+           f"oracle port, extrapolated linearly to all {cfg.q} lambdas")
+    if bounded:
+        txt += ("; a step is one fold's sample inside the pool (K steps = ceil(K / k) rounds of k concurrent folds, "
+                "~150 s together); when the rounds would not fit, a fold's Hessian is assembled from a fraction of "
+                "its training rows (assemble_row_fraction per step) and that time scaled linearly to all rows")
+    return txt
 
 
 def run_reference(args, cfg, world, rank):
@@ -317,11 +343,30 @@ def run_reference(args, cfg, world, rank):
     Xw, Yw = configs.generate(warm)
     for _ in range(args.warmup):  # page in BLAS, scipy and the thread pool on a small problem
         cpu_fold_threads(warm, Xw, Yw, 1)
-    vals, details, cores = [], [], 1
-    for _ in range(args.steps):
-        v, cores, det = cpu_fold_threads(cfg, X, Y, args.cpu_lams)
-        vals.append(v)
-        details.append(det)
+    # A step is one fold's sample inside the fold thread pool: the pool runs all k folds concurrently (one BLAS thread
+    # each, so every sample sees the mode's contention), and K steps take ceil(K / k) rounds of the pool -- about
+    # REF_BUDGET_S of CPU time together. When the rounds would not fit, the assembly of a fold's Hessian (linear in
+    # its rows, most of a sample) runs on a fraction of the rows and is scaled, calibrated round by round.
+    cores = min(cfg.k, cpu_cores())
+    waves = -(-cfg.k // cpu_cores())
+    rounds = -(-max(args.steps, 1) // cfg.k)
+    frac = 1.0 if REF_BUDGET_S / rounds >= 45.0 else min(1.0, max(0.05, (REF_BUDGET_S / rounds - 20.0) / 25.0))
+    vals, details = [], []
+    t_start = time.perf_counter()
+    for rd in range(rounds):
+        res, wall = cpu_fold_round(cfg, X, Y, args.cpu_lams, frac)
+        # the sweep of this mode ends with its slowest fold: every step of a round carries the round's rate
+        round_value = cfg.k * cfg.q / (waves * max(r[0] + cfg.q * r[1] for r in res))
+        for f, (setup, lam, t_asm, fr) in enumerate(res):
+            if len(vals) < args.steps:
+                vals.append(round_value)
+                details.append({"round": rd, "fold": f, "t_setup_s": setup, "t_lambda_s": lam, "round_wall_s": wall,
+                                "t_assemble_timed_s": t_asm, "assemble_row_fraction": fr})
+        if rd + 1 < rounds:  # time left per round = rest (Choleskys, fit, lambdas) + fraction x full assembly
+            left = (REF_BUDGET_S - (time.perf_counter() - t_start)) / (rounds - rd - 1)
+            t_asm = max(r[2] for r in res)
+            full_asm = t_asm / min(r[3] for r in res)
+            frac = min(1.0, max(0.05, (left - (wall - t_asm)) / full_asm))
     value = float(np.mean(vals))
     out = {
         "impl": "reference",
@@ -339,7 +384,7 @@ def run_reference(args, cfg, world, rank):
         "data": "synthetic (seeded generator, paper_1404_0466_b200/configs.py)",
         "config": config_dict(cfg, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": fold_thread_sample_text(cfg, args.cpu_lams), "steps": details,
+                         "sample": fold_thread_sample_text(cfg, args.cpu_lams, bounded=True), "steps": details,
                          "host": host_info(), "modes": cpu_modes(cfg.name)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
