@@ -685,9 +685,9 @@ def run_ours(args, cfg, world, rank, local):
         "stages": stages,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu_val, cores, det = cpu_fold_threads(cfg, X, Y, 1)
+        cpu_val, cores, det = cpu_fold_threads(cfg, X, Y, args.cpu_lams)  # the reference arm's sample, once
         out["cpu_baseline"] = {"value": cpu_val, "unit": UNIT, "cores": cores, "kind": "port",
-                               "sample": fold_thread_sample_text(cfg, 1), **det, "host": host_info(),
+                               "sample": fold_thread_sample_text(cfg, args.cpu_lams), **det, "host": host_info(),
                                "modes": cpu_modes(cfg.name)}
     if rank == 0:
         print(json.dumps(out), flush=True)
